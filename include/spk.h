@@ -1,0 +1,121 @@
+/* spk.h - C-ABI of the B200-native stage-parallel Radau IIA hot path (libspk, sm_100a).
+ *
+ * Every entry point takes plain pointers and sizes; device pointers are fp64 CUDA buffers in the
+ * reference layout: a level's DoFs are C-order (x slowest) n_ax^dim nodes, stage/block vectors
+ * are stacked (nblk, n) with an element stride. All calls are ordered on the caller's stream
+ * (cudaStream_t passed as void*). Return value: SPK_OK or one of the error codes below; the text
+ * of the last error of the calling thread is in spk_last_error().
+ *
+ * Which reference interface each entry point replaces (file:line under the reference package
+ * pkg/src/spirk/):
+ *   spk_ctx_create          GridHierarchy.__init__ / build_hierarchy      fem.py:75-102, :300
+ *   spk_level_info          GridLevel.n_per_axis/n_dofs/h                 fem.py:44-69
+ *   spk_nodes_1d            GridLevel.axis_coords                         fem.py:68-69
+ *   spk_stage_apply         (D_M (x) M + D_K (x) K) u, K1 stage operator   fem.py:120-151 + SPEC irk:A
+ *   spk_block_apply         apply_shifted / apply_constrained             fem.py:145-170
+ *   spk_pair_apply          PairBlockSolver._apply                        multigrid.py:292-304
+ *   spk_residual            _VCycleBase._cycle r = b - A x               multigrid.py:122
+ *   spk_cheb_init/step      ChebyshevSmoother.apply                       multigrid.py:74-88
+ *   spk_pair_residual/cheb  PairBlockSolver smoothing (2x2 block Jacobi)  multigrid.py:306-313
+ *   spk_dinv_norm           estimate_lambda_max inner step                multigrid.py:45-62
+ *   spk_transfer            prolong / restrict (+ mask, + accumulate)     fem.py:189-211, multigrid.py:171-177
+ *   spk_combine             SPEC tensor_ops dense_combine (D (x) I) u
+ *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
+ *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
+ *   spk_mask                GridHierarchy.constrain                       fem.py:153-158
+ */
+#ifndef SPK_H_
+#define SPK_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPK_OK 0
+#define SPK_EDIM 1          /* DimensionMismatchError */
+#define SPK_ECONFIG 2       /* ConfigurationError */
+#define SPK_ENUMERIC 3      /* NumericalFailureError */
+#define SPK_ESPECTRAL 4     /* SpectralFailureError */
+#define SPK_ECUDA 5         /* CUDA runtime failure */
+#define SPK_ECOMM 6         /* collective failure */
+#define SPK_EUNSUPPORTED 7  /* degree / stage count without a compiled kernel */
+
+typedef struct spk_ctx spk_ctx;
+
+int spk_version(void);
+const char* spk_last_error(void);
+
+/* host-side discretisation data (no GPU needed) */
+int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out);
+int spk_ctx_destroy(spk_ctx* ctx);
+int spk_level_info(const spk_ctx* ctx, int level, int* n_per_axis, long long* n_dofs, double* h,
+                   int* n_elems);
+int spk_level_tables(const spk_ctx* ctx, int level, double* Me, double* Ke);
+int spk_nodes_1d(const spk_ctx* ctx, int level, double* out);
+int spk_prolong_table(const spk_ctx* ctx, double* P);
+int spk_apply_smem(int degree, int Q);
+int spk_set_chunks(spk_ctx* ctx, int target_ctas);
+
+/* K1: v_i = sum_j (DM_ij M + DK_ij K) u_j, Q stages, DM/DK row-major Q x Q host arrays */
+int spk_stage_apply(spk_ctx* ctx, int level, int Q, const double* DM, const double* DK, int constrained,
+                    const double* u, long long su, double* v, long long sv, void* stream);
+/* K1 on an x-slab with halo planes: the local array has x_elems elements along x (K*x_elems+1
+ * planes); only nodes of elements [ex_begin, ex_end) (+ the last plane if store_last) are written */
+int spk_stage_apply_slab(spk_ctx* ctx, int level, int Q, const double* DM, const double* DK,
+                         const double* u, long long su, double* v, long long sv, int x_elems,
+                         int ex_begin, int ex_end, int store_last, void* stream);
+/* v_b = lam_b M u_b + tau K u_b for b < nblk (lams: nblk host values, or 1 if lam_uniform) */
+int spk_block_apply(spk_ctx* ctx, int level, int nblk, const double* lams, int lam_uniform, double tau,
+                    int constrained, const double* u, long long su, double* v, long long sv,
+                    void* stream);
+/* pair operator [[K',-M'],[M',K']] on (2, n): K' = re M + tau K, M' = im M */
+int spk_pair_apply(spk_ctx* ctx, int level, double re, double im, double tau, int constrained,
+                   const double* u, double* v, void* stream);
+
+/* smoother building blocks (block mode: per-block lam / Chebyshev coefficients) */
+int spk_residual(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* x,
+                 const double* b, double* r, double* d_out, const double* c2s, void* stream);
+int spk_cheb_init(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* cs,
+                  const double* b, double* r, double* x, double* d, void* stream);
+int spk_cheb_step(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* c1s,
+                  const double* c2s, const double* d_in, double* r, double* x, double* d_out,
+                  void* stream);
+int spk_pair_residual(spk_ctx* ctx, int level, double re, double im, double tau, const double* x,
+                      const double* b, double* r, double* d_out, double c2, void* stream);
+int spk_pair_cheb_init(spk_ctx* ctx, int level, double re, double im, double tau, double c,
+                       const double* b, double* r, double* x, double* d, void* stream);
+int spk_pair_cheb_step(spk_ctx* ctx, int level, double re, double im, double tau, double c1, double c2,
+                       const double* d_in, double* r, double* x, double* d_out, void* stream);
+/* power iteration step: w = Dinv A u, *norm_dev = ||w||_2 (device scalar); pair != 0 uses (re, im) */
+int spk_dinv_norm(spk_ctx* ctx, int level, int pair, double lam_or_re, double im, double tau,
+                  const double* u, double* w, double* norm_dev, void* stream);
+
+/* transfers: prolong (coarse level -> level) or restrict (level -> level-1) for nblk blocks */
+int spk_transfer(spk_ctx* ctx, int level, int nblk, int prolong, const double* in, double* out,
+                 double* scratch, int accumulate, int mask, void* stream);
+int spk_axpy_flag(long long total, double* x, const double* d, int* flag, void* stream);
+
+/* (D (x) I) u with D row-major nout x nin (host); mask_level >= 0 zeroes its boundary nodes */
+int spk_combine(spk_ctx* ctx, int mask_level, long long n, int nin, int nout, const double* D,
+                const double* in, long long sin, double* out, long long sout, int accumulate,
+                void* stream);
+
+/* GMRES: w -= (*h_prev) v_prev ; *out = <v_cur, w>  (v_cur == NULL: *out = ||w||) */
+int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
+            const double* v_cur, double* out, void* stream);
+int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);
+int spk_lincomb(long long n, int k, const double* const* vs_dev, const double* y_dev, double* z,
+                void* stream);
+
+/* separable fields and the stage right-hand side */
+int spk_outer3(spk_ctx* ctx, int level, const double* g1_dev, double* out, void* stream);
+int spk_rhs(spk_ctx* ctx, int level, int Q, const double* g1_dev, const double* T, const double* Ainv,
+            const double* ku, double* out, void* stream);
+int spk_update(long long n, int Q, const double* k, const double* bw_dev, double tau, double* u,
+               void* stream);
+int spk_mask(spk_ctx* ctx, int level, int nblk, double* u, double value, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPK_H_ */

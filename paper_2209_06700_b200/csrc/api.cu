@@ -1,0 +1,651 @@
+// C-ABI host layer of libspk: discretisation setup (Q_k element tables on GLL nodes, transfer
+// tables, per-level dims) and stream-ordered kernel launches. See include/spk.h for the contract.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/spk.h"
+#include "spk_internal.cuh"
+#include "spk_vecops.cuh"
+
+struct spk_ctx {
+  int dim = 0, max_level = 0, K = 0;
+  std::vector<SpkDims> dims;
+  std::vector<SpkTab> tabs;
+  std::vector<double> h;
+  double xi[SPK_KMAX + 1];
+  double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
+  int target_ctas = 0;    // 0: automatic x-chunking
+  // device scratch (lazily allocated on first device call)
+  double* partial = nullptr;
+  unsigned* counter = nullptr;
+  int partial_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SPK_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ---- 1D reference element on [0,1]: GLL nodes, Gauss rule, Lagrange basis ----
+void gll_nodes(int K, double* xi) {
+  // Gauss-Lobatto-Legendre points mapped to [0,1] (closed forms for K <= 4)
+  switch (K) {
+    case 1: xi[0] = 0.0; xi[1] = 1.0; break;
+    case 2: xi[0] = 0.0; xi[1] = 0.5; xi[2] = 1.0; break;
+    case 3: {
+      const double a = std::sqrt(5.0) / 10.0;
+      xi[0] = 0.0; xi[1] = 0.5 - a; xi[2] = 0.5 + a; xi[3] = 1.0;
+      break;
+    }
+    case 4: {
+      const double a = std::sqrt(21.0) / 14.0;
+      xi[0] = 0.0; xi[1] = 0.5 - a; xi[2] = 0.5; xi[3] = 0.5 + a; xi[4] = 1.0;
+      break;
+    }
+  }
+}
+
+void gauss_legendre01(int m, double* x, double* w) {
+  // Newton on P_m, mapped to [0,1]
+  for (int i = 0; i < m; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (m + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= m; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (m == 1) { p1 = z; p0 = 1.0; }
+      const double dp = m * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    double p0 = 1.0, p1 = z;
+    for (int k = 2; k <= m; ++k) {
+      const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    const double dp = (m == 1) ? 1.0 : m * (z * p1 - p0) / (z * z - 1.0);
+    x[m - 1 - i] = 0.5 * (z + 1.0);
+    w[m - 1 - i] = 1.0 / ((1.0 - z * z) * dp * dp);  // weight on [0,1] = 2/((1-z^2)P'^2) / 2
+  }
+  if (m == 1) { x[0] = 0.5; w[0] = 1.0; }
+}
+
+double lagr(const double* xi, int K, int a, double x) {
+  double v = 1.0;
+  for (int m = 0; m <= K; ++m)
+    if (m != a) v *= (x - xi[m]) / (xi[a] - xi[m]);
+  return v;
+}
+
+double lagr_d(const double* xi, int K, int a, double x) {
+  double s = 0.0;
+  for (int m = 0; m <= K; ++m) {
+    if (m == a) continue;
+    double t = 1.0 / (xi[a] - xi[m]);
+    for (int l = 0; l <= K; ++l)
+      if (l != a && l != m) t *= (x - xi[l]) / (xi[a] - xi[l]);
+    s += t;
+  }
+  return s;
+}
+
+SpkDims dims_of(const spk_ctx* c, int level) { return c->dims[level]; }
+
+int check_level(const spk_ctx* c, int level) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (level < 0 || level > c->max_level)
+    return fail(SPK_ECONFIG, "level " + std::to_string(level) + " outside hierarchy");
+  return SPK_OK;
+}
+
+int ensure_scratch(spk_ctx* c, int need) {
+  if (c->partial_cap >= need && c->counter) return SPK_OK;
+  if (c->partial) cudaFree(c->partial);
+  if (!c->counter) {
+    cudaError_t e = cudaMalloc(&c->counter, 64 * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counter)");
+    e = cudaMemset(c->counter, 0, 64 * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(counter)");
+  }
+  int cap = need < (1 << 16) ? (1 << 16) : need;
+  cudaError_t e = cudaMalloc(&c->partial, (size_t)cap * sizeof(double));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(partial)");
+  c->partial_cap = cap;
+  return SPK_OK;
+}
+
+// x-chunking of the sliding window: enough CTAs to fill every SM about twice
+void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb) {
+  static const int TYE[5] = {0, 16, 8, 5, 4}, TZE[5] = {0, 32, 16, 11, 8};
+  const int gz = (a.g.Ez + 1 + TZE[K] - 1) / TZE[K];
+  const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + TYE[K] - 1) / TYE[K];
+  const long long tiles = (long long)gz * gy * nb;
+  if (a.g.Ex == 0) { a.nchunks = 1; a.xe_chunk = 1; a.ex_begin = 0; a.ex_end = 0; return; }
+  if (a.ex_end <= a.ex_begin) { a.ex_begin = 0; a.ex_end = a.g.Ex; }
+  const int nel = a.ex_end - a.ex_begin;
+  const long long target = c->target_ctas > 0 ? c->target_ctas : 2 * 148 * 2;
+  long long nch = (target + tiles - 1) / tiles;
+  if (nch < 1) nch = 1;
+  if (nch > nel) nch = nel;
+  // keep at least 4 elements per chunk (the chunk pays one halo element)
+  while (nch > 1 && nel / nch < 4) --nch;
+  a.xe_chunk = (int)((nel + nch - 1) / nch);
+  a.nchunks = (nel + a.xe_chunk - 1) / a.xe_chunk;
+}
+
+SpkApplyArgs base_args(const spk_ctx* c, int level) {
+  SpkApplyArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = c->dims[level];
+  a.t = c->tabs[level];
+  a.store_last = 1;
+  return a;
+}
+
+int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a, cudaStream_t s,
+                 int* nctas = nullptr) {
+  cudaError_t e = spk_launch_apply(c->K, Q, block_mode, epi, a, s, nctas);
+  if (e != cudaSuccess) return cuda_fail(e, "stage_apply launch");
+  return SPK_OK;
+}
+
+int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, int lam_uniform,
+                         double tau, int constrained, int epi, SpkApplyArgs a, cudaStream_t s,
+                         const double* c1s, const double* c2s) {
+  // launch in groups of SPK_BMAX blocks so per-block coefficients fit the parameter block
+  for (int b0 = 0; b0 < nblk; b0 += (lam_uniform && !c1s && !c2s) ? nblk : SPK_BMAX) {
+    const int nb = (lam_uniform && !c1s && !c2s) ? nblk : std::min(SPK_BMAX, nblk - b0);
+    a.blk_base = b0;
+    a.nblk = nb;
+    a.lam_uniform = lam_uniform;
+    a.tau = tau;
+    a.constrained = constrained;
+    for (int i = 0; i < (lam_uniform ? 1 : nb); ++i) a.lam[i] = lams[b0 + i];
+    for (int i = 0; i < nb && i < SPK_BMAX; ++i) {
+      a.c1[i] = c1s ? c1s[b0 + i] : 0.0;
+      a.c2[i] = c2s ? c2s[b0 + i] : 0.0;
+    }
+    set_chunking(c, a, c->K, nb);
+    // blocks are addressed as blk*su from the base pointer, so pass the unshifted base
+    int rc = launch_apply(c, 1, true, epi, a, s);
+    if (rc) return rc;
+  }
+  return SPK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spk_version(void) { return 1; }
+
+const char* spk_last_error(void) { return g_err.c_str(); }
+
+int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
+  if (!out) return fail(SPK_ECONFIG, "null output pointer");
+  if (dim < 1 || dim > 3) return fail(SPK_ECONFIG, "dim must be 1, 2 or 3, got " + std::to_string(dim));
+  if (degree < 1 || degree > SPK_KMAX)
+    return fail(SPK_EUNSUPPORTED, "degree must be in [1, 4], got " + std::to_string(degree));
+  if (max_level < 1 || max_level > 10)
+    return fail(SPK_ECONFIG, "max_level must be in [1, 10], got " + std::to_string(max_level));
+  spk_ctx* c = new spk_ctx();
+  c->dim = dim;
+  c->max_level = max_level;
+  c->K = degree;
+  const int K = degree;
+  gll_nodes(K, c->xi);
+  // reference element matrices with the exact (K+1)-point Gauss rule
+  double gx[SPK_KMAX + 1], gw[SPK_KMAX + 1];
+  gauss_legendre01(K + 1, gx, gw);
+  double Mh[SPK_KMAX + 1][SPK_KMAX + 1] = {}, Kh[SPK_KMAX + 1][SPK_KMAX + 1] = {};
+  for (int a = 0; a <= K; ++a)
+    for (int b = 0; b <= K; ++b) {
+      double m = 0.0, k = 0.0;
+      for (int q = 0; q <= K; ++q) {
+        m += gw[q] * lagr(c->xi, K, a, gx[q]) * lagr(c->xi, K, b, gx[q]);
+        k += gw[q] * lagr_d(c->xi, K, a, gx[q]) * lagr_d(c->xi, K, b, gx[q]);
+      }
+      Mh[a][b] = m;
+      Kh[a][b] = k;
+    }
+  // symmetrise (exact symmetry of the element matrices)
+  for (int a = 0; a <= K; ++a)
+    for (int b = a + 1; b <= K; ++b) {
+      Mh[b][a] = Mh[a][b];
+      Kh[b][a] = Kh[a][b];
+    }
+  // prolongation table: fine local position f in [0, 2K] of a coarse element
+  std::memset(c->P, 0, sizeof(c->P));
+  for (int f = 0; f <= 2 * K; ++f) {
+    const double pos = (f <= K) ? 0.5 * c->xi[f] : 0.5 + 0.5 * c->xi[f - K];
+    for (int j = 0; j <= K; ++j) {
+      double v = lagr(c->xi, K, j, pos);
+      if (f == 0) v = (j == 0) ? 1.0 : 0.0;
+      if (f == 2 * K) v = (j == K) ? 1.0 : 0.0;
+      if (f == K && K % 2 == 0) v = (j == K / 2) ? 1.0 : 0.0;  // midpoint is a coarse node
+      c->P[f * (SPK_KMAX + 1) + j] = v;
+    }
+  }
+  for (int l = 0; l <= max_level; ++l) {
+    const int N = 1 << l;
+    const int nax = K * N + 1;
+    SpkDims g;
+    g.nz = nax; g.Ez = N;
+    g.ny = dim >= 2 ? nax : 1; g.Ey = dim >= 2 ? N : 0;
+    g.nx = dim >= 3 ? nax : 1; g.Ex = dim >= 3 ? N : 0;
+    g.n = (long long)g.nx * g.ny * g.nz;
+    const double h = 1.0 / N;
+    SpkTab t;
+    std::memset(&t, 0, sizeof(t));
+    for (int a = 0; a <= K; ++a)
+      for (int b = 0; b <= K; ++b) {
+        t.Me[a][b] = h * Mh[a][b];
+        t.Ke[a][b] = Kh[a][b] / h;
+      }
+    c->dims.push_back(g);
+    c->tabs.push_back(t);
+    c->h.push_back(h);
+  }
+  *out = c;
+  return SPK_OK;
+}
+
+int spk_ctx_destroy(spk_ctx* c) {
+  if (!c) return SPK_OK;
+  if (c->partial) cudaFree(c->partial);
+  if (c->counter) cudaFree(c->counter);
+  delete c;
+  return SPK_OK;
+}
+
+int spk_level_info(const spk_ctx* c, int level, int* n_per_axis, long long* n_dofs, double* h,
+                   int* n_elems) {
+  if (int rc = check_level(c, level)) return rc;
+  const SpkDims& g = c->dims[level];
+  if (n_per_axis) *n_per_axis = g.nz;
+  if (n_dofs) *n_dofs = g.n;
+  if (h) *h = c->h[level];
+  if (n_elems) *n_elems = g.Ez;
+  return SPK_OK;
+}
+
+int spk_level_tables(const spk_ctx* c, int level, double* Me, double* Ke) {
+  if (int rc = check_level(c, level)) return rc;
+  const int K = c->K;
+  for (int a = 0; a <= K; ++a)
+    for (int b = 0; b <= K; ++b) {
+      if (Me) Me[a * (K + 1) + b] = c->tabs[level].Me[a][b];
+      if (Ke) Ke[a * (K + 1) + b] = c->tabs[level].Ke[a][b];
+    }
+  return SPK_OK;
+}
+
+int spk_nodes_1d(const spk_ctx* c, int level, double* out) {
+  if (int rc = check_level(c, level)) return rc;
+  const int K = c->K, N = c->dims[level].Ez;
+  const double h = c->h[level];
+  for (int e = 0; e < N; ++e)
+    for (int r = 0; r < K; ++r) out[K * e + r] = (e + c->xi[r]) * h;
+  out[K * N] = 1.0;
+  out[0] = 0.0;
+  return SPK_OK;
+}
+
+int spk_prolong_table(const spk_ctx* c, double* P) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  const int K = c->K;
+  for (int f = 0; f <= 2 * K; ++f)
+    for (int j = 0; j <= K; ++j) P[f * (K + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
+  return SPK_OK;
+}
+
+int spk_apply_smem(int degree, int Q) { return spk_apply_smem_bytes(degree, Q); }
+
+int spk_set_chunks(spk_ctx* c, int target_ctas) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  c->target_ctas = target_ctas;
+  return SPK_OK;
+}
+
+int spk_stage_apply(spk_ctx* c, int level, int Q, const double* DM, const double* DK, int constrained,
+                    const double* u, long long su, double* v, long long sv, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  if (Q < 1 || Q > SPK_QMAX)
+    return fail(SPK_EUNSUPPORTED, "fused stage operator supports Q in [1, 4], got " + std::to_string(Q));
+  SpkApplyArgs a = base_args(c, level);
+  a.u = u; a.v = v; a.su = su; a.sv = sv;
+  a.constrained = constrained;
+  for (int i = 0; i < Q; ++i)
+    for (int j = 0; j < Q; ++j) {
+      a.DM[i][j] = DM[i * Q + j];
+      a.DK[i][j] = DK[i * Q + j];
+    }
+  set_chunking(c, a, c->K, 1);
+  return launch_apply(c, Q, false, EPI_STORE, a, (cudaStream_t)stream);
+}
+
+int spk_stage_apply_slab(spk_ctx* c, int level, int Q, const double* DM, const double* DK,
+                         const double* u, long long su, double* v, long long sv, int x_elems,
+                         int ex_begin, int ex_end, int store_last, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  if (c->dim != 3) return fail(SPK_ECONFIG, "slab windows need a 3D hierarchy");
+  if (Q < 1 || Q > SPK_QMAX)
+    return fail(SPK_EUNSUPPORTED, "fused stage operator supports Q in [1, 4], got " + std::to_string(Q));
+  if (x_elems < 1 || ex_begin < 0 || ex_end > x_elems || ex_begin >= ex_end)
+    return fail(SPK_ECONFIG, "bad slab element window");
+  SpkApplyArgs a = base_args(c, level);
+  a.g.Ex = x_elems;
+  a.g.nx = c->K * x_elems + 1;
+  a.g.n = (long long)a.g.nx * a.g.ny * a.g.nz;
+  a.u = u; a.v = v; a.su = su; a.sv = sv;
+  a.ex_begin = ex_begin; a.ex_end = ex_end; a.store_last = store_last;
+  for (int i = 0; i < Q; ++i)
+    for (int j = 0; j < Q; ++j) {
+      a.DM[i][j] = DM[i * Q + j];
+      a.DK[i][j] = DK[i * Q + j];
+    }
+  set_chunking(c, a, c->K, 1);
+  return launch_apply(c, Q, false, EPI_STORE, a, (cudaStream_t)stream);
+}
+
+int spk_block_apply(spk_ctx* c, int level, int nblk, const double* lams, int lam_uniform, double tau,
+                    int constrained, const double* u, long long su, double* v, long long sv,
+                    void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  if (nblk < 1) return SPK_OK;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = u; a.v = v; a.su = su; a.sv = sv;
+  return apply_blocks_chunked(c, level, nblk, lams, lam_uniform, tau, constrained, EPI_STORE, a,
+                              (cudaStream_t)stream, nullptr, nullptr);
+}
+
+int spk_pair_apply(spk_ctx* c, int level, double re, double im, double tau, int constrained,
+                   const double* u, double* v, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = u; a.v = v; a.su = n; a.sv = n;
+  a.constrained = constrained;
+  a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
+  a.DK[0][0] = tau; a.DK[1][1] = tau;
+  set_chunking(c, a, c->K, 1);
+  return launch_apply(c, 2, false, EPI_STORE, a, (cudaStream_t)stream);
+}
+
+int spk_residual(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* x,
+                 const double* b, double* r, double* d_out, const double* c2s, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = x; a.su = n; a.b = b; a.r = r; a.d_out = d_out; a.se = n;
+  return apply_blocks_chunked(c, level, nblk, lams, 0, tau, 1, EPI_RESID, a, (cudaStream_t)stream,
+                              nullptr, d_out ? c2s : nullptr);
+}
+
+int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* cs,
+                  const double* b, double* r, double* x, double* d, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
+    const int nb = std::min(SPK_BMAX, nblk - b0);
+    SpkVecArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.g = c->dims[level];
+    a.t = c->tabs[level];
+    a.nblk = nb; a.blk_base = 0; a.constrained = 1; a.pair = 0; a.lam_uniform = 0;
+    a.tau = tau;
+    for (int i = 0; i < nb; ++i) { a.lam[i] = lams[b0 + i]; a.c[i] = cs[b0 + i]; }
+    const long long off = (long long)b0 * a.g.n;
+    a.in0 = b + off; a.out0 = r + off; a.out1 = x + off; a.out2 = d + off;
+    cudaError_t e = spk_launch_cheb_init(c->K, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cheb_init");
+  }
+  return SPK_OK;
+}
+
+int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
+                  const double* c2s, const double* d_in, double* r, double* x, double* d_out,
+                  void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = d_in; a.su = n; a.r = r; a.x = x; a.d_out = d_out; a.se = n;
+  return apply_blocks_chunked(c, level, nblk, lams, 0, tau, 1, EPI_CHEB, a, (cudaStream_t)stream, c1s,
+                              c2s);
+}
+
+int spk_pair_residual(spk_ctx* c, int level, double re, double im, double tau, const double* x,
+                      const double* b, double* r, double* d_out, double c2, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = x; a.su = n; a.b = b; a.r = r; a.d_out = d_out; a.se = n;
+  a.constrained = 1;
+  a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
+  a.DK[0][0] = tau; a.DK[1][1] = tau;
+  a.tau = tau; a.jre = re; a.jim = im; a.c2[0] = c2;
+  set_chunking(c, a, c->K, 1);
+  return launch_apply(c, 2, false, EPI_RESID, a, (cudaStream_t)stream);
+}
+
+int spk_pair_cheb_init(spk_ctx* c, int level, double re, double im, double tau, double cc,
+                       const double* b, double* r, double* x, double* d, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  SpkVecArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = c->dims[level];
+  a.t = c->tabs[level];
+  a.nblk = 2; a.constrained = 1; a.pair = 1;
+  a.tau = tau; a.jre = re; a.jim = im; a.c[0] = cc;
+  a.in0 = b; a.out0 = r; a.out1 = x; a.out2 = d;
+  cudaError_t e = spk_launch_cheb_init(c->K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "pair cheb_init");
+  return SPK_OK;
+}
+
+int spk_pair_cheb_step(spk_ctx* c, int level, double re, double im, double tau, double c1, double c2,
+                       const double* d_in, double* r, double* x, double* d_out, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = d_in; a.su = n; a.r = r; a.x = x; a.d_out = d_out; a.se = n;
+  a.constrained = 1;
+  a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
+  a.DK[0][0] = tau; a.DK[1][1] = tau;
+  a.tau = tau; a.jre = re; a.jim = im; a.c1[0] = c1; a.c2[0] = c2;
+  set_chunking(c, a, c->K, 1);
+  return launch_apply(c, 2, false, EPI_CHEB, a, (cudaStream_t)stream);
+}
+
+int spk_dinv_norm(spk_ctx* c, int level, int pair, double lam_or_re, double im, double tau,
+                  const double* u, double* w, double* norm_dev, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs a = base_args(c, level);
+  a.u = u; a.v = w; a.su = n; a.sv = n;
+  a.constrained = 1;
+  a.tau = tau;
+  int nctas = 0;
+  // size the partial buffer conservatively before launching
+  if (int rc = ensure_scratch(c, 1 << 16)) return rc;
+  a.partial = c->partial;
+  int rc;
+  if (!pair) {
+    a.nblk = 1; a.blk_base = 0; a.lam_uniform = 1; a.lam[0] = lam_or_re;
+    set_chunking(c, a, c->K, 1);
+    rc = launch_apply(c, 1, true, EPI_DINV, a, (cudaStream_t)stream, &nctas);
+  } else {
+    a.DM[0][0] = lam_or_re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = lam_or_re;
+    a.DK[0][0] = tau; a.DK[1][1] = tau;
+    a.jre = lam_or_re; a.jim = im;
+    set_chunking(c, a, c->K, 1);
+    rc = launch_apply(c, 2, false, EPI_DINV, a, (cudaStream_t)stream, &nctas);
+  }
+  if (rc) return rc;
+  if (nctas > c->partial_cap) return fail(SPK_ECUDA, "partial buffer too small");
+  cudaError_t e = spk_launch_reduce_partials(c->partial, nctas, norm_dev, 1, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_partials");
+  return SPK_OK;
+}
+
+int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in, double* out,
+                 double* scratch, int accumulate, int mask, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  if (level < 1) return fail(SPK_ECONFIG, "transfer needs level >= 1");
+  const SpkDims gf = c->dims[level], gc = c->dims[level - 1];
+  const int nf = gf.nz, nc = gc.nz, Nc = gc.Ez;
+  const int dim = c->dim;
+  // sweep order z (last axis), y, x; arrays are [nblk][x][y][z]
+  // current shape (per block): sizes along (x, y, z)
+  int sx = prolong ? (dim >= 3 ? nc : 1) : (dim >= 3 ? nf : 1);
+  int sy = prolong ? (dim >= 2 ? nc : 1) : (dim >= 2 ? nf : 1);
+  int sz = prolong ? nc : nf;
+  const int tz = prolong ? nf : nc;
+  const long long out_scratch_max = (long long)nblk * (long long)nf * nf * (dim >= 3 ? nf : 1);
+  (void)out_scratch_max;
+  // scratch holds two ping-pong intermediates
+  double* bufA = scratch;
+  double* bufB = scratch + (long long)nblk * (dim >= 3 ? (long long)nf * nf * nf : (long long)nf * nf);
+  const double* src = in;
+  SpkTransferArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.Nc = Nc;
+  a.prolong = prolong;
+  for (int f = 0; f <= 2 * c->K; ++f)
+    for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
+  const SpkDims gout = prolong ? gf : gc;
+  int nsweeps = dim;
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    const bool last = (sw == nsweeps - 1);
+    double* dst = last ? out : (sw % 2 == 0 ? bufA : bufB);
+    a.in = src;
+    a.out = dst;
+    a.accumulate = last ? accumulate : 0;
+    a.mask = last ? mask : 0;
+    a.g = gout;
+    if (sw == 0) {  // z axis
+      a.outer = (long long)nblk * sx * sy; a.inner = 1; a.nin = sz; a.nout = tz;
+      sz = tz;
+    } else if (sw == 1) {  // y axis
+      const int ty = prolong ? nf : nc;
+      a.outer = (long long)nblk * sx; a.inner = sz; a.nin = sy; a.nout = ty;
+      sy = ty;
+    } else {  // x axis
+      const int tx = prolong ? nf : nc;
+      a.outer = nblk; a.inner = (long long)sy * sz; a.nin = sx; a.nout = tx;
+      sx = tx;
+    }
+    cudaError_t e = spk_launch_transfer(c->K, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "transfer");
+    src = dst;
+  }
+  return SPK_OK;
+}
+
+int spk_axpy_flag(long long total, double* x, const double* d, int* flag, void* stream) {
+  cudaError_t e = spk_launch_axpy_flag(total, x, d, flag, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "axpy_flag");
+  return SPK_OK;
+}
+
+int spk_combine(spk_ctx* c, int mask_level, long long n, int nin, int nout, const double* D,
+                const double* in, long long sin, double* out, long long sout, int accumulate,
+                void* stream) {
+  if (nin < 1 || nout < 1 || nin > SPK_CMAX || nout > SPK_CMAX)
+    return fail(SPK_EUNSUPPORTED, "combine supports up to 18 rows/columns");
+  SpkCombineArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.in = in; a.out = out; a.n = n; a.sin = sin; a.sout = sout;
+  a.nin = nin; a.nout = nout; a.accumulate = accumulate;
+  if (mask_level >= 0) {
+    if (int rc = check_level(c, mask_level)) return rc;
+    a.mask = 1;
+    a.g = c->dims[mask_level];
+  }
+  for (int o = 0; o < nout; ++o)
+    for (int j = 0; j < nin; ++j) a.D[o * SPK_CMAX + j] = D[o * nin + j];
+  cudaError_t e = spk_launch_combine(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "combine");
+  return SPK_OK;
+}
+
+int spk_mgs(spk_ctx* c, long long n, double* w, const double* v_prev, const double* h_prev,
+            const double* v_cur, double* out, void* stream) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (int rc = ensure_scratch(c, spk_mgs_grid())) return rc;
+  SpkMgsArgs a;
+  a.n = n; a.w = w; a.v_prev = v_prev; a.h_prev = h_prev; a.v_cur = v_cur; a.out = out;
+  a.partial = c->partial; a.counter = c->counter;
+  cudaError_t e = spk_launch_mgs(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mgs");
+  return SPK_OK;
+}
+
+int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream) {
+  cudaError_t e = spk_launch_scale_div(n, w, h, v, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "scale_div");
+  return SPK_OK;
+}
+
+int spk_lincomb(long long n, int k, const double* const* vs_dev, const double* y_dev, double* z,
+                void* stream) {
+  cudaError_t e = spk_launch_lincomb(n, k, vs_dev, y_dev, z, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lincomb");
+  return SPK_OK;
+}
+
+int spk_outer3(spk_ctx* c, int level, const double* g1_dev, double* out, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  SpkSepArgs a;
+  a.g = c->dims[level]; a.gx = g1_dev; a.out = out;
+  cudaError_t e = spk_launch_outer3(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "outer3");
+  return SPK_OK;
+}
+
+int spk_rhs(spk_ctx* c, int level, int Q, const double* g1_dev, const double* T, const double* Ainv,
+            const double* ku, double* out, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  if (Q < 1 || Q > SPK_CMAX) return fail(SPK_EUNSUPPORTED, "rhs: bad Q");
+  SpkRhsArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = c->dims[level]; a.gx = g1_dev; a.ku = ku; a.out = out; a.Q = Q;
+  for (int j = 0; j < Q; ++j) a.T[j] = T[j];
+  for (int i = 0; i < Q; ++i)
+    for (int j = 0; j < Q; ++j) a.Ainv[i * SPK_CMAX + j] = Ainv[i * Q + j];
+  cudaError_t e = spk_launch_rhs(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "rhs");
+  return SPK_OK;
+}
+
+int spk_update(long long n, int Q, const double* k, const double* bw_dev, double tau, double* u,
+               void* stream) {
+  cudaError_t e = spk_launch_update(n, Q, k, bw_dev, tau, u, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "update");
+  return SPK_OK;
+}
+
+int spk_mask(spk_ctx* c, int level, int nblk, double* u, double value, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const SpkDims g = c->dims[level];
+  cudaError_t e = spk_launch_mask((long long)nblk * g.n, g, u, value, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mask");
+  return SPK_OK;
+}
+
+}  // extern "C"

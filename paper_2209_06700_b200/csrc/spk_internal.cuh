@@ -1,0 +1,69 @@
+// Internal declarations shared by the sm_100a kernels and the C-ABI host layer.
+//
+// Layout contract (reference fem.py:124, 213-218): a level's DoFs are a
+// C-order (x slowest, z fastest) tensor of n_ax^dim nodes; stage/block vectors are stacked
+// (nblk, n) with a stage stride. Degenerate axes (dim < 3) are represented as axes of one
+// node and zero elements, so one 3D kernel family serves dim = 1, 2, 3.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define SPK_KMAX 4       // highest Q_k degree with a compiled kernel
+#define SPK_QMAX 4       // highest stage count of the fused stage-coupled kernel
+#define SPK_BMAX 16      // per-launch block-parameter slots (block mode)
+#define SPK_THREADS 256
+
+struct SpkDims {
+  int nx, ny, nz;   // nodes per axis (1 for a degenerate axis)
+  int Ex, Ey, Ez;   // elements per axis (0 for a degenerate axis)
+  long long n;      // nx*ny*nz
+};
+
+// 1D element tables of one level, scaled by h (mass) and 1/h (stiffness), and the per-node
+// diagonal pattern of the assembled 1D matrices.
+struct SpkTab {
+  double Me[SPK_KMAX + 1][SPK_KMAX + 1];
+  double Ke[SPK_KMAX + 1][SPK_KMAX + 1];
+};
+
+enum SpkEpi {
+  EPI_STORE = 0,   // v = Op(u)                      (boundary rows: identity if constrained)
+  EPI_RESID = 1,   // r = b - Op(u); optionally d = c2 * Dinv r
+  EPI_CHEB = 2,    // fused Chebyshev step on (r, x, d)
+  EPI_DINV = 3,    // w = Dinv * Op(u)  + sum of squares (power iteration)
+};
+
+struct SpkApplyArgs {
+  const double* u;        // operator input (stage/block q at u + q*su)
+  double* v;              // output (EPI_STORE / EPI_DINV)
+  long long su, sv;
+  SpkDims g;
+  int xe_chunk, nchunks;  // x-chunking of the sliding window
+  int ex_begin, ex_end;   // element range in x whose nodes are produced (slab windows)
+  int store_last;         // also produce the last vertex plane when ex_end == Ex
+  int constrained;
+  int nblk;               // block mode: number of independent blocks
+  int blk_base;           // block mode: index of the first block of this launch
+  // coupled mode: v_i = sum_j DM_ij M u_j + DK_ij K u_j
+  double DM[SPK_QMAX][SPK_QMAX];
+  double DK[SPK_QMAX][SPK_QMAX];
+  // block mode: v_b = lam_b M u_b + tau K u_b   (lam_uniform: lam[0] for every block)
+  double lam[SPK_BMAX];
+  int lam_uniform;
+  double tau;
+  SpkTab t;
+  // epilogue operands
+  const double* b;        // EPI_RESID: rhs
+  double* r;              // EPI_RESID out / EPI_CHEB in-out residual
+  double* x;              // EPI_CHEB in-out iterate
+  double* d_out;          // EPI_CHEB new search direction; EPI_RESID optional d
+  long long se;           // stage stride of epilogue operands
+  double c1[SPK_BMAX], c2[SPK_BMAX];  // Chebyshev coefficients per block (pair: slot 0)
+  // Jacobi diagonal: block mode diag = lam_b*dm + tau*dk ; pair mode uses (re, im, tau)
+  double jre, jim;
+  double* partial;        // EPI_DINV: per-CTA partial sums (deterministic reduction)
+};
+
+// launchers (stage_apply.cu)
+cudaError_t spk_launch_apply(int K, int Q, bool block_mode, int epi, const SpkApplyArgs& a,
+                             cudaStream_t s, int* nctas_out);

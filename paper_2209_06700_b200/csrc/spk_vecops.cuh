@@ -1,0 +1,84 @@
+// Argument blocks of the memory-bound kernels (vecops.cu).
+#pragma once
+#include "spk_internal.cuh"
+
+#define SPK_CMAX 18   // max rows/cols of a stage-combine matrix (2*ceil(9/2) = 10 real rows)
+
+struct SpkVecArgs {
+  SpkDims g;
+  SpkTab t;
+  int nblk, blk_base, constrained, pair, lam_uniform;
+  double lam[SPK_BMAX];
+  double tau, jre, jim;
+  double c[SPK_BMAX];
+  const double* in0;
+  double* out0;
+  double* out1;
+  double* out2;
+};
+
+struct SpkTransferArgs {
+  const double* in;
+  double* out;
+  long long outer, inner;
+  int nin, nout;
+  int Nc;         // coarse elements along the axis
+  int prolong;    // 1: coarse -> fine, 0: restriction (transpose)
+  int accumulate; // out += result
+  int mask;       // zero boundary nodes of level g (final sweep)
+  SpkDims g;
+  double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
+};
+
+struct SpkCombineArgs {
+  const double* in;
+  double* out;
+  long long n, sin, sout;
+  int nin, nout, mask, accumulate;
+  SpkDims g;
+  double D[SPK_CMAX * SPK_CMAX];
+};
+
+struct SpkMgsArgs {
+  long long n;
+  double* w;
+  const double* v_prev;
+  const double* h_prev;
+  const double* v_cur;
+  double* out;
+  double* partial;
+  unsigned* counter;
+};
+
+struct SpkSepArgs {
+  SpkDims g;
+  const double* gx;
+  double* out;
+};
+
+struct SpkRhsArgs {
+  SpkDims g;
+  const double* gx;     // 1D load vector of the separable spatial factor
+  const double* ku;     // K u_n
+  double* out;          // (Q, n)
+  int Q;
+  double T[SPK_CMAX];   // time factors T(t_n + c_j tau)
+  double Ainv[SPK_CMAX * SPK_CMAX];
+};
+
+cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s);
+cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s);
+cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);
+cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s);
+int spk_mgs_grid();
+cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
+cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s);
+cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s);
+cudaError_t spk_launch_lincomb(long long n, int k, const double* const* vs, const double* y, double* z,
+                               cudaStream_t s);
+cudaError_t spk_launch_outer3(const SpkSepArgs& a, cudaStream_t s);
+cudaError_t spk_launch_rhs(const SpkRhsArgs& a, cudaStream_t s);
+cudaError_t spk_launch_update(long long n, int Q, const double* k, const double* bw, double tau, double* u,
+                              cudaStream_t s);
+cudaError_t spk_launch_mask(long long total, const SpkDims& g, double* u, double value, cudaStream_t s);
+int spk_apply_smem_bytes(int K, int Q);

@@ -1,0 +1,574 @@
+// K1: batched / stage-coupled matrix-free Q_k operator on the uniform grid, sm_100a, fp64.
+//
+//   coupled mode : v_i = sum_j ( DM_ij M + DK_ij K ) u_j        i,j < Q      (I(x)M + tau A(x)K, ...)
+//   block mode   : v_b = lam_b M u_b + tau K u_b                 b < nblk     (lam M + tau K per block)
+//
+// M = Mx(x)My(x)Mz and K = Kx My Mz + Mx Ky Mz + Mx My Kz are the Kronecker forms the reference
+// applies with dense 1D contractions (fem.py:120-151, _contract fem.py:37-41). Here the assembled
+// 1D matrices are never formed: each axis is applied element-by-element from the (k+1)x(k+1)
+// element tables, which gives the flop-minimal banded form (SURVEY.md §7 hard part 1).
+//
+// Schedule ("2.5D sliding window", one CTA = one (y,z) tile x one x-chunk, all Q stages):
+//   per x-plane:  cp.async plane x+1 into the other smem buffer (double buffering)
+//                 Z-phase   a = Mz u, b = Kz u                 (smem -> smem, register-blocked)
+//                 Y-phase   ma = My a, c = Ky a + My b          (smem -> smem)
+//                 X-phase   stage mix p_i = sum_j DM_ij ma_j + DK_ij c_j, q_i = sum_j DK_ij ma_j
+//                           and element-push accumulation v += Mx[.,r] p + Kx[.,r] q in registers
+//   an element's K output planes are finished when its last plane arrives -> fused epilogue.
+// HBM traffic per apply: read u once (+ L2-resident halo), write v once = 16 B per stage-DoF.
+#include "spk_internal.cuh"
+
+namespace {
+
+template <int K> struct Tile;
+template <> struct Tile<1> { static constexpr int TYE = 16, TZE = 32; };
+template <> struct Tile<2> { static constexpr int TYE = 8, TZE = 16; };
+template <> struct Tile<3> { static constexpr int TYE = 5, TZE = 11; };
+template <> struct Tile<4> { static constexpr int TYE = 4, TZE = 8; };
+
+template <int K, int Q> struct Geo {
+  static constexpr int TYE = Tile<K>::TYE, TZE = Tile<K>::TZE;
+  static constexpr int TY = K * TYE, TZ = K * TZE;
+  static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
+  static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
+  static constexpr int TZp = TZ | 1;
+  static constexpr int U_SZ = Q * NYin * NZp;          // one plane buffer
+  static constexpr int AB_SZ = Q * NYin * TZp;
+  static constexpr int MC_SZ = Q * TY * TZp;
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * AB_SZ + 2 * MC_SZ;
+  static constexpr int PPT = (TY * TZ + SPK_THREADS - 1) / SPK_THREADS;
+};
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// assembled 1D diagonal at node i of an axis with E elements (E == 0: degenerate axis)
+template <int K>
+__device__ __forceinline__ void diag1(const SpkTab& t, int i, int E, double& dm, double& dk) {
+  if (E == 0) { dm = 1.0; dk = 0.0; return; }
+  const int e = i / K, r = i - e * K;
+  if (r != 0) { dm = t.Me[r][r]; dk = t.Ke[r][r]; return; }
+  dm = 0.0; dk = 0.0;
+  if (e > 0) { dm += t.Me[K][K]; dk += t.Ke[K][K]; }
+  if (e < E) { dm += t.Me[0][0]; dk += t.Ke[0][0]; }
+}
+
+// diag(lam M + tau K) pieces at a node, same association order as the reference's
+// np.multiply.outer chain (fem.py:172-187)
+template <int K>
+__device__ __forceinline__ void node_diag(const SpkTab& t, const SpkDims& g, int x, int y, int z,
+                                          double& dm, double& dk) {
+  double mx, kx, my, ky, mz, kz;
+  diag1<K>(t, x, g.Ex, mx, kx);
+  diag1<K>(t, y, g.Ey, my, ky);
+  diag1<K>(t, z, g.Ez, mz, kz);
+  dm = (mx * my) * mz;
+  dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+}
+
+__device__ __forceinline__ bool on_boundary(const SpkDims& g, int x, int y, int z) {
+  return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+         (g.Ez > 0 && (z == 0 || z == g.nz - 1));
+}
+
+// One element-wise 1D application of two tables on the same input:
+//   vertex r=0 gathers the left element (row K) and the right element (row 0);
+//   interior r>=1 use the right element only.
+template <int K>
+__device__ __forceinline__ void elem2(const double (&L)[K + 1], const double (&R)[K + 1], double wl,
+                                      double wr, const double (&E1)[SPK_KMAX + 1][SPK_KMAX + 1],
+                                      const double (&E2)[SPK_KMAX + 1][SPK_KMAX + 1], double (&o1)[K],
+                                      double (&o2)[K]) {
+  double l1 = 0.0, l2 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+  for (int s = 0; s <= K; ++s) {
+    l1 = fma(E1[K][s], L[s], l1);
+    l2 = fma(E2[K][s], L[s], l2);
+    r1 = fma(E1[0][s], R[s], r1);
+    r2 = fma(E2[0][s], R[s], r2);
+  }
+  o1[0] = wl * l1 + wr * r1;
+  o2[0] = wl * l2 + wr * r2;
+#pragma unroll
+  for (int r = 1; r < K; ++r) {
+    double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      a1 = fma(E1[r][s], R[s], a1);
+      a2 = fma(E2[r][s], R[s], a2);
+    }
+    o1[r] = a1;
+    o2[r] = a2;
+  }
+}
+
+// y-sweep on two inputs: ma = M a ; c = K a + M b
+template <int K>
+__device__ __forceinline__ void elem3(const double (&La)[K + 1], const double (&Ra)[K + 1],
+                                      const double (&Lb)[K + 1], const double (&Rb)[K + 1], double wl,
+                                      double wr, const SpkTab& t, double (&ma)[K], double (&c)[K]) {
+  double lm = 0.0, lc = 0.0, rm = 0.0, rc = 0.0;
+#pragma unroll
+  for (int s = 0; s <= K; ++s) {
+    lm = fma(t.Me[K][s], La[s], lm);
+    lc = fma(t.Ke[K][s], La[s], lc);
+    lc = fma(t.Me[K][s], Lb[s], lc);
+    rm = fma(t.Me[0][s], Ra[s], rm);
+    rc = fma(t.Ke[0][s], Ra[s], rc);
+    rc = fma(t.Me[0][s], Rb[s], rc);
+  }
+  ma[0] = wl * lm + wr * rm;
+  c[0] = wl * lc + wr * rc;
+#pragma unroll
+  for (int r = 1; r < K; ++r) {
+    double am = 0.0, ac = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      am = fma(t.Me[r][s], Ra[s], am);
+      ac = fma(t.Ke[r][s], Ra[s], ac);
+      ac = fma(t.Me[r][s], Rb[s], ac);
+    }
+    ma[r] = am;
+    c[r] = ac;
+  }
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, int x, int y, int z,
+                                         const double (&val)[Q], double& sumsq) {
+  const SpkDims& g = a.g;
+  const long long gi = ((long long)x * g.ny + y) * g.nz + z;
+  const bool bnd = a.constrained && on_boundary(g, x, y, z);
+  const long long ubase = BLOCK ? (long long)blk * a.su : 0;
+  const long long ebase = BLOCK ? (long long)blk * a.se : 0;
+  const int slot = BLOCK ? blk - a.blk_base : 0;
+  double Av[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) Av[q] = bnd ? __ldg(a.u + ubase + q * a.su + gi) : val[q];
+
+  if constexpr (EPI == EPI_STORE) {
+    const long long vbase = BLOCK ? (long long)blk * a.sv : 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) a.v[vbase + q * a.sv + gi] = Av[q];
+  } else {
+    // Jacobi diagonal (analytic; reference operator_diagonal fem.py:172-187, 1.0 on boundary)
+    double dm, dk;
+    node_diag<K>(a.t, g, x, y, z, dm, dk);
+    if constexpr (EPI == EPI_DINV) {
+      if constexpr (BLOCK || Q == 1) {
+        const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
+        const double inv = bnd ? 1.0 : 1.0 / (lam * dm + a.tau * dk);
+        const double w = inv * Av[0];
+        const long long vbase = BLOCK ? (long long)blk * a.sv : 0;
+        a.v[vbase + gi] = w;
+        sumsq = fma(w, w, sumsq);
+      } else {  // pair 2x2 block Jacobi (multigrid.py:268-276, 306-313)
+        const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
+        const double db = bnd ? 0.0 : a.jim * dm;
+        const double det = da * da + db * db;
+        const double A_ = da / det, B_ = db / det;
+        const double w0 = A_ * Av[0] + B_ * Av[1];
+        const double w1 = -B_ * Av[0] + A_ * Av[1];
+        a.v[gi] = w0;
+        a.v[a.sv + gi] = w1;
+        sumsq = fma(w0, w0, sumsq);
+        sumsq = fma(w1, w1, sumsq);
+      }
+    } else {
+      double rn[Q];
+      if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          rn[q] = __ldg(a.b + ebase + q * a.se + gi) - Av[q];
+          a.r[ebase + q * a.se + gi] = rn[q];
+        }
+      } else {  // EPI_CHEB:  x += d ; r -= A d ; d = c1 d + c2 Dinv r   (multigrid.py:82-87)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double dq = __ldg(a.u + ubase + q * a.su + gi);
+          rn[q] = a.r[ebase + q * a.se + gi] - Av[q];
+          a.r[ebase + q * a.se + gi] = rn[q];
+          a.x[ebase + q * a.se + gi] = a.x[ebase + q * a.se + gi] + dq;
+        }
+      }
+      if (a.d_out != nullptr) {
+        const double c2 = a.c2[slot];
+        double z0[Q];
+        if constexpr (BLOCK || Q == 1) {
+          const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
+          const double inv = bnd ? 1.0 : 1.0 / (lam * dm + a.tau * dk);
+          z0[0] = inv * rn[0];
+        } else {
+          const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
+          const double db = bnd ? 0.0 : a.jim * dm;
+          const double det = da * da + db * db;
+          const double A_ = da / det, B_ = db / det;
+          z0[0] = A_ * rn[0] + B_ * rn[1];
+          if constexpr (Q > 1) z0[1] = -B_ * rn[0] + A_ * rn[1];
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          double dn;
+          if constexpr (EPI == EPI_CHEB) {
+            const double dq = __ldg(a.u + ubase + q * a.su + gi);
+            dn = a.c1[slot] * dq + c2 * z0[q];
+          } else {
+            dn = z0[q] / c2;  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
+          }
+          a.d_out[ebase + q * a.se + gi] = dn;
+        }
+      }
+    }
+  }
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+__global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
+    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
+  using G = Geo<K, Q>;
+  constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ;
+  constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
+  constexpr int PPT = G::PPT;
+
+  extern __shared__ double smem[];
+  double* Us = smem;                    // [2][Q][NYin][NZp]
+  double* As = Us + 2 * G::U_SZ;        // [Q][NYin][TZp]
+  double* Bs = As + G::AB_SZ;
+  double* MAs = Bs + G::AB_SZ;          // [Q][TY][TZp]
+  double* Cs = MAs + G::MC_SZ;
+
+  const int tid = threadIdx.x;
+  const SpkDims g = a.g;
+  const bool ydeg = (g.Ey == 0), xdeg = (g.Ex == 0);
+  const int ez0 = blockIdx.x * TZE, ey0 = blockIdx.y * TYE;
+  const int chunk = blockIdx.z % a.nchunks;
+  const int blk = BLOCK ? (a.blk_base + (int)(blockIdx.z / a.nchunks)) : 0;
+
+  const int z_lo = K * ez0, z_hi = min(K * (ez0 + TZE), g.nz);
+  const int y_lo = ydeg ? 0 : K * ey0, y_hi = ydeg ? 1 : min(K * (ey0 + TYE), g.ny);
+  const int nzo = z_hi - z_lo, nyo = y_hi - y_lo;
+  const int nez = min(TZE, g.Ez + 1 - ez0);            // includes the virtual last-vertex element
+  const int ney = ydeg ? 1 : min(TYE, g.Ey + 1 - ey0);
+  const double* __restrict__ u = a.u + (BLOCK ? (long long)blk * a.su : 0);
+
+  // block mode coefficients
+  double lamb = 0.0;
+  if constexpr (BLOCK) lamb = a.lam_uniform ? a.lam[0] : a.lam[blk - a.blk_base];
+
+  // x-chunk (elements [ex0, ex1)); planes K*(ex0-1) .. K*ex1
+  int ex0 = 0, ex1 = 0, xs = 0, nplanes = 1, ecur = 0;
+  if (!xdeg) {
+    ex0 = a.ex_begin + chunk * a.xe_chunk;
+    ex1 = min(a.ex_end, ex0 + a.xe_chunk);
+    ecur = ex0 > 0 ? ex0 - 1 : 0;
+    xs = K * ecur;
+    nplanes = K * ex1 - xs + 1;
+  }
+
+  const int yy_lo = ydeg ? K : 0, yy_hi = ydeg ? K + 1 : NYin;
+
+  auto load_plane = [&](int x, int buf) {
+    double* dst = Us + buf * G::U_SZ;
+    const long long xoff = (long long)x * g.ny;
+    const bool xb = a.constrained && !xdeg && (x == 0 || x == g.nx - 1);
+    for (int idx = tid; idx < Q * NYin * NZin; idx += SPK_THREADS) {
+      const int q = idx / (NYin * NZin);
+      const int rem = idx - q * (NYin * NZin);
+      const int yy = rem / NZin, zz = rem - yy * NZin;
+      const int gy = y_lo - K + yy, gz = z_lo - K + zz;
+      bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
+      if (in && a.constrained)
+        in = !(xb || (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1);
+      const double* src = in ? u + (long long)q * a.su + (xoff + gy) * g.nz + gz : u;
+      cp_async8(dst + (q * NYin + yy) * NZp + zz, src, in ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+
+  // Z/Y work partition: segments of consecutive elements per item so loads are reused
+  const int zrows = yy_hi - yy_lo;
+  const int nsegz = max(1, min(nez, SPK_THREADS / (Q * zrows)));
+  const int lenz = (nez + nsegz - 1) / nsegz;
+  const int nsegy = ydeg ? 1 : max(1, min(ney, SPK_THREADS / (Q * max(nzo, 1))));
+  const int leny = (ney + nsegy - 1) / nsegy;
+
+  // X-phase state
+  double acc[PPT][Q][K + 1];
+  int pyl[PPT], pzl[PPT];
+  bool pv[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int p = tid + j * SPK_THREADS;
+    pyl[j] = p / TZ;
+    pzl[j] = p - pyl[j] * TZ;
+    pv[j] = (p < TY * TZ) && pyl[j] < nyo && pzl[j] < nzo;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) acc[j][q][s] = 0.0;
+  }
+  double sumsq = 0.0;
+
+  load_plane(xs, 0);
+  int buf = 0;
+  for (int pl = 0; pl < nplanes; ++pl) {
+    const int x = xs + pl;
+    cp_async_wait_all();
+    __syncthreads();
+    if (pl + 1 < nplanes) load_plane(x + 1, buf ^ 1);
+
+    // ---------------- Z-phase: a = Mz u, b = Kz u on rows [yy_lo, yy_hi) ----------------
+    {
+      const double* Ub = Us + buf * G::U_SZ;
+      for (int it = tid; it < Q * zrows * nsegz; it += SPK_THREADS) {
+        const int yy = yy_lo + it % zrows;
+        const int rest = it / zrows;
+        const int seg = rest % nsegz, q = rest / nsegz;
+        const int e_beg = seg * lenz, e_end = min(nez, e_beg + lenz);
+        if (e_beg >= e_end) continue;
+        const double* row = Ub + (q * NYin + yy) * NZp;
+        double* arow = As + (q * NYin + yy) * TZp;
+        double* brow = Bs + (q * NYin + yy) * TZp;
+        double L[K + 1], R[K + 1];
+#pragma unroll
+        for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
+        for (int el = e_beg; el < e_end; ++el) {
+          R[0] = L[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) R[s] = row[K * el + K + s];
+          const int ez = ez0 + el;
+          const double wl = ez > 0 ? 1.0 : 0.0, wr = ez < g.Ez ? 1.0 : 0.0;
+          double oa[K], ob[K];
+          elem2<K>(L, R, wl, wr, a.t.Me, a.t.Ke, oa, ob);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int zl = K * el + r;
+            if (zl < nzo) { arow[zl] = oa[r]; brow[zl] = ob[r]; }
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) L[s] = R[s];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- Y-phase: ma = My a, c = Ky a + My b ----------------
+    if (ydeg) {
+      for (int it = tid; it < Q * nzo; it += SPK_THREADS) {
+        const int q = it / nzo, zl = it - q * nzo;
+        MAs[(q * TY) * TZp + zl] = As[(q * NYin + K) * TZp + zl];
+        Cs[(q * TY) * TZp + zl] = Bs[(q * NYin + K) * TZp + zl];
+      }
+    } else {
+      for (int it = tid; it < Q * nzo * nsegy; it += SPK_THREADS) {
+        const int zl = it % nzo;
+        const int rest = it / nzo;
+        const int seg = rest % nsegy, q = rest / nsegy;
+        const int e_beg = seg * leny, e_end = min(ney, e_beg + leny);
+        if (e_beg >= e_end) continue;
+        const double* acol = As + (q * NYin) * TZp + zl;
+        const double* bcol = Bs + (q * NYin) * TZp + zl;
+        double La[K + 1], Ra[K + 1], Lb[K + 1], Rb[K + 1];
+#pragma unroll
+        for (int s = 0; s <= K; ++s) {
+          La[s] = acol[(K * e_beg + s) * TZp];
+          Lb[s] = bcol[(K * e_beg + s) * TZp];
+        }
+        for (int el = e_beg; el < e_end; ++el) {
+          Ra[0] = La[K];
+          Rb[0] = Lb[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) {
+            Ra[s] = acol[(K * el + K + s) * TZp];
+            Rb[s] = bcol[(K * el + K + s) * TZp];
+          }
+          const int ey = ey0 + el;
+          const double wl = ey > 0 ? 1.0 : 0.0, wr = ey < g.Ey ? 1.0 : 0.0;
+          double om[K], oc[K];
+          elem3<K>(La, Ra, Lb, Rb, wl, wr, a.t, om, oc);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int yl = K * el + r;
+            if (yl < nyo) {
+              MAs[(q * TY + yl) * TZp + zl] = om[r];
+              Cs[(q * TY + yl) * TZp + zl] = oc[r];
+            }
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- X-phase: stage mix + element-push accumulation ----------------
+    const int r_loc = xdeg ? 0 : x - K * ecur;   // local plane index within element ecur (0..K)
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (!pv[j]) continue;
+      const int yl = pyl[j], zl = pzl[j];
+      double ma[Q], cc[Q], pq[Q], qq[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        ma[q] = MAs[(q * TY + yl) * TZp + zl];
+        cc[q] = Cs[(q * TY + yl) * TZp + zl];
+      }
+      if constexpr (BLOCK) {
+        pq[0] = lamb * ma[0] + a.tau * cc[0];
+        qq[0] = a.tau * ma[0];
+      } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          double p = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < Q; ++jj) {
+            p = fma(a.DM[i][jj], ma[jj], p);
+            p = fma(a.DK[i][jj], cc[jj], p);
+            s2 = fma(a.DK[i][jj], ma[jj], s2);
+          }
+          pq[i] = p;
+          qq[i] = s2;
+        }
+      }
+      const int y = y_lo + yl, z = z_lo + zl;
+      if (xdeg) {
+        epilogue<K, Q, BLOCK, EPI>(a, blk, 0, y, z, pq, sumsq);
+        continue;
+      }
+      // accumulate this plane as local node r_loc of element ecur
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+#pragma unroll
+        for (int rr = 0; rr <= K; ++rr) {
+          if (rr == r_loc) {
+#pragma unroll
+            for (int s = 0; s <= K; ++s)
+              acc[j][q][s] = fma(a.t.Me[s][rr], pq[q], fma(a.t.Ke[s][rr], qq[q], acc[j][q][s]));
+          }
+        }
+      }
+      if (r_loc == K) {
+        // element ecur complete: nodes K*ecur + s, s < K
+        if (ecur >= ex0) {
+#pragma unroll
+          for (int s = 0; s < K; ++s) {
+            double val[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
+            epilogue<K, Q, BLOCK, EPI>(a, blk, K * ecur + s, y, z, val, sumsq);
+          }
+        }
+        if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
+          double val[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
+          epilogue<K, Q, BLOCK, EPI>(a, blk, K * g.Ex, y, z, val, sumsq);
+        }
+        // carry the shared vertex and start the next element with this plane as its local 0
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double carry = acc[j][q][K];
+#pragma unroll
+          for (int s = 0; s <= K; ++s)
+            acc[j][q][s] = fma(a.t.Me[s][0], pq[q], a.t.Ke[s][0] * qq[q]);
+          acc[j][q][0] += carry;
+        }
+      }
+    }
+    if (!xdeg && r_loc == K) ++ecur;
+    buf ^= 1;
+  }
+
+  if constexpr (EPI == EPI_DINV) {
+    // deterministic per-CTA partial: fixed-shape tree in shared memory
+    __syncthreads();
+    double* red = smem;
+    red[tid] = sumsq;
+    __syncthreads();
+    for (int off = SPK_THREADS / 2; off > 0; off >>= 1) {
+      if (tid < off) red[tid] += red[tid + off];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      a.partial[cta] = red[0];
+    }
+  }
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
+  using G = Geo<K, Q>;
+  const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
+  static bool configured = false;
+  auto kern = stage_apply_kernel<K, Q, BLOCK, EPI>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int gz = (a.g.Ez + 1 + G::TZE - 1) / G::TZE;
+  const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + G::TYE - 1) / G::TYE;
+  const int nb = BLOCK ? a.nblk : 1;
+  dim3 grid(gz, gy, a.nchunks * nb);
+  if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
+  kern<<<grid, SPK_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t dispatch_k(int Q, bool block_mode, int epi, const SpkApplyArgs& a, cudaStream_t s, int* n) {
+  if (block_mode) {
+    switch (epi) {
+      case EPI_STORE: return launch_one<K, 1, true, EPI_STORE>(a, s, n);
+      case EPI_RESID: return launch_one<K, 1, true, EPI_RESID>(a, s, n);
+      case EPI_CHEB: return launch_one<K, 1, true, EPI_CHEB>(a, s, n);
+      case EPI_DINV: return launch_one<K, 1, true, EPI_DINV>(a, s, n);
+    }
+    return cudaErrorInvalidValue;
+  }
+  switch (Q) {
+    case 1: return launch_one<K, 1, false, EPI_STORE>(a, s, n);
+    case 2:
+      switch (epi) {
+        case EPI_STORE: return launch_one<K, 2, false, EPI_STORE>(a, s, n);
+        case EPI_RESID: return launch_one<K, 2, false, EPI_RESID>(a, s, n);
+        case EPI_CHEB: return launch_one<K, 2, false, EPI_CHEB>(a, s, n);
+        case EPI_DINV: return launch_one<K, 2, false, EPI_DINV>(a, s, n);
+      }
+      return cudaErrorInvalidValue;
+    case 3: return launch_one<K, 3, false, EPI_STORE>(a, s, n);
+    case 4: return launch_one<K, 4, false, EPI_STORE>(a, s, n);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t spk_launch_apply(int K, int Q, bool block_mode, int epi, const SpkApplyArgs& a,
+                             cudaStream_t s, int* nctas_out) {
+  switch (K) {
+    case 1: return dispatch_k<1>(Q, block_mode, epi, a, s, nctas_out);
+    case 2: return dispatch_k<2>(Q, block_mode, epi, a, s, nctas_out);
+    case 3: return dispatch_k<3>(Q, block_mode, epi, a, s, nctas_out);
+    case 4: return dispatch_k<4>(Q, block_mode, epi, a, s, nctas_out);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int spk_apply_smem_bytes(int K, int Q) {
+  switch (K * 16 + Q) {
+#define SPK_CASE(k, q) case k * 16 + q: return (int)(sizeof(double) * Geo<k, q>::SMEM_DOUBLES);
+    SPK_CASE(1, 1) SPK_CASE(1, 2) SPK_CASE(1, 3) SPK_CASE(1, 4)
+    SPK_CASE(2, 1) SPK_CASE(2, 2) SPK_CASE(2, 3) SPK_CASE(2, 4)
+    SPK_CASE(3, 1) SPK_CASE(3, 2) SPK_CASE(3, 3) SPK_CASE(3, 4)
+    SPK_CASE(4, 1) SPK_CASE(4, 2) SPK_CASE(4, 3) SPK_CASE(4, 4)
+#undef SPK_CASE
+  }
+  return -1;
+}

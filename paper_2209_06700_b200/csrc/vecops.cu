@@ -1,0 +1,409 @@
+// Memory-bound companion kernels of the device solver stack (sm_100a, fp64):
+//   * grid transfers P / P^T along one axis (reference fem.py:189-211, _prolongation_1d :287-297)
+//   * Chebyshev start / finish steps (multigrid.py:74-88)
+//   * stage combine (D (x) I) u  (SPEC tensor_ops dense_combine; eq. irk:A/irk:P basis changes)
+//   * GMRES modified Gram-Schmidt step = fused axpy + dot with a deterministic reduction
+//     (krylov.py:74-82), device-resident Hessenberg entries (no host round trip per dot)
+//   * RHS assembly for separable sources and nodal interpolation (fem.py:220-246, :368-372)
+#include <cmath>
+
+#include "spk_internal.cuh"
+#include "spk_vecops.cuh"
+
+namespace {
+
+constexpr int TPB = 256;
+
+template <int K>
+__device__ __forceinline__ void dk_diag1(const double* Me, const double* Ke, int i, int E, double& dm,
+                                         double& dk) {
+  constexpr int P = SPK_KMAX + 1;
+  if (E == 0) { dm = 1.0; dk = 0.0; return; }
+  const int e = i / K, r = i - e * K;
+  if (r != 0) { dm = Me[r * P + r]; dk = Ke[r * P + r]; return; }
+  dm = 0.0; dk = 0.0;
+  if (e > 0) { dm += Me[K * P + K]; dk += Ke[K * P + K]; }
+  if (e < E) { dm += Me[0]; dk += Ke[0]; }
+}
+
+__device__ __forceinline__ void decompose(long long gi, const SpkDims& g, int& x, int& y, int& z) {
+  z = (int)(gi % g.nz);
+  long long t = gi / g.nz;
+  y = (int)(t % g.ny);
+  x = (int)(t / g.ny);
+}
+
+__device__ __forceinline__ bool bnd3(const SpkDims& g, int x, int y, int z) {
+  return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+         (g.Ez > 0 && (z == 0 || z == g.nz - 1));
+}
+
+template <int K>
+__device__ __forceinline__ void nodediag(const SpkVecArgs& a, int x, int y, int z, double& dm,
+                                         double& dk) {
+  double mx, kx, my, ky, mz, kz;
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], x, a.g.Ex, mx, kx);
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], y, a.g.Ey, my, ky);
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], z, a.g.Ez, mz, kz);
+  dm = (mx * my) * mz;
+  dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+}
+
+// ---- Chebyshev start: r = b ; x = 0 ; d = c2 * Dinv r   (block or pair Jacobi) ----
+template <int K>
+__global__ void cheb_init_kernel(const __grid_constant__ SpkVecArgs a) {
+  const long long n = a.g.n;
+  const long long total = (long long)a.nblk * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / n);
+    const long long gi = i - (long long)b * n;
+    int x, y, z;
+    decompose(gi, a.g, x, y, z);
+    const bool bnd = a.constrained && bnd3(a.g, x, y, z);
+    double dm, dk;
+    nodediag<K>(a, x, y, z, dm, dk);
+    if (!a.pair) {
+      const int slot = b - a.blk_base;
+      const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
+      const double inv = bnd ? 1.0 : 1.0 / (lam * dm + a.tau * dk);
+      const double r = a.in0[i];
+      a.out0[i] = r;
+      a.out1[i] = 0.0;
+      a.out2[i] = (inv * r) / a.c[slot];  // c = theta (multigrid.py:77)
+    } else if (b == 0) {
+      // pair: blocks 0/1 are (re, im) of one complex block
+      const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
+      const double db = bnd ? 0.0 : a.jim * dm;
+      const double det = da * da + db * db;
+      const double A_ = da / det, B_ = db / det;
+      const double r0 = a.in0[gi], r1 = a.in0[n + gi];
+      a.out0[gi] = r0; a.out0[n + gi] = r1;
+      a.out1[gi] = 0.0; a.out1[n + gi] = 0.0;
+      a.out2[gi] = (A_ * r0 + B_ * r1) / a.c[0];
+      a.out2[n + gi] = (-B_ * r0 + A_ * r1) / a.c[0];
+    }
+  }
+}
+
+// ---- x += d with a non-finite flag (V-cycle NaN check, multigrid.py:127-128) ----
+__global__ void axpy_flag_kernel(long long total, double* x, const double* d, int* flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = x[i] + d[i];
+    x[i] = v;
+    bad |= !isfinite(v);
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---- one-axis transfer: view arrays as [outer][n_axis][inner] ----
+template <int K>
+__global__ void transfer_axis_kernel(const __grid_constant__ SpkTransferArgs a) {
+  constexpr int P2 = 2 * SPK_KMAX + 1;
+  const long long total = a.outer * (long long)a.nout * a.inner;
+  for (long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x; gid < total;
+       gid += (long long)gridDim.x * blockDim.x) {
+    const long long in_idx = gid % a.inner;
+    const long long rest = gid / a.inner;
+    const int i = (int)(rest % a.nout);
+    const long long o = rest / a.nout;
+    const double* src = a.in + o * (long long)a.nin * a.inner + in_idx;
+    double val = 0.0;
+    if (a.prolong) {
+      // fine node i <- coarse element ec, local fine position f in [0, 2K]
+      const int Nc = a.Nc;
+      const int ec = min(i / (2 * K), Nc - 1);
+      const int f = i - 2 * K * ec;
+#pragma unroll
+      for (int j = 0; j <= K; ++j) val = fma(a.P[f * (SPK_KMAX + 1) + j], src[(long long)(K * ec + j) * a.inner], val);
+    } else {
+      // coarse node J = K*ec + r gathers P^T
+      const int Nc = a.Nc;
+      const int ec = i / K, r = i - ec * K;
+      if (r != 0) {
+#pragma unroll
+        for (int f = 1; f < 2 * K; ++f)
+          val = fma(a.P[f * (SPK_KMAX + 1) + r], src[(long long)(2 * K * ec + f) * a.inner], val);
+      } else {
+        val = src[(long long)(2 * K * ec) * a.inner];  // coincident fine vertex, weight 1
+        if (ec < Nc) {
+#pragma unroll
+          for (int f = 1; f < 2 * K; ++f)
+            val = fma(a.P[f * (SPK_KMAX + 1) + 0], src[(long long)(2 * K * ec + f) * a.inner], val);
+        }
+        if (ec > 0) {
+#pragma unroll
+          for (int f = 1; f < 2 * K; ++f)
+            val = fma(a.P[f * (SPK_KMAX + 1) + K], src[(long long)(2 * K * (ec - 1) + f) * a.inner], val);
+        }
+      }
+    }
+    (void)P2;
+    const long long oidx = (o * a.nout + i) * a.inner + in_idx;
+    if (a.mask) {
+      const long long gi = oidx % a.g.n;
+      int x, y, z;
+      decompose(gi, a.g, x, y, z);
+      if (bnd3(a.g, x, y, z)) val = 0.0;
+    }
+    if (a.accumulate) a.out[oidx] += val;
+    else a.out[oidx] = val;
+  }
+}
+
+// ---- (D (x) I) u : out_i = sum_j D_ij in_j (pointwise, all stages in registers) ----
+__global__ void combine_kernel(const __grid_constant__ SpkCombineArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double in[SPK_CMAX];
+#pragma unroll
+    for (int j = 0; j < SPK_CMAX; ++j)
+      if (j < a.nin) in[j] = a.in[j * a.sin + i];
+    for (int o = 0; o < a.nout; ++o) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < SPK_CMAX; ++j)
+        if (j < a.nin) s = fma(a.D[o * SPK_CMAX + j], in[j], s);
+      if (a.mask) {
+        int x, y, z;
+        decompose(i, a.g, x, y, z);
+        if (bnd3(a.g, x, y, z)) s = 0.0;
+      }
+      a.out[o * a.sout + i] = a.accumulate ? a.out[o * a.sout + i] + s : s;
+    }
+  }
+}
+
+// ---- deterministic block reduction helper ----
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int tid = threadIdx.x;
+  red[tid] = v;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (tid < off) red[tid] += red[tid + off];
+    __syncthreads();
+  }
+  return red[0];
+}
+
+// last-CTA-done finalisation: sums per-CTA partials in CTA order (run-to-run deterministic)
+__device__ void finalize_partials(double mine, double* partial, unsigned* counter, double* out,
+                                  int sqrt_out, double* red) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = mine;
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += ((volatile double*)partial)[b];
+  const double tot = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    *out = sqrt_out ? sqrt(tot) : tot;
+    *counter = 0u;
+  }
+}
+
+// ---- MGS step: w -= h_prev * v_prev ; out = <v_cur, w> (or ||w|| if v_cur == null) ----
+__global__ void mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
+  __shared__ double red[TPB];
+  double s = 0.0;
+  const double h = a.v_prev ? *a.h_prev : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double w = a.w[i];
+    if (a.v_prev) {
+      w = w - h * a.v_prev[i];
+      a.w[i] = w;
+    }
+    const double c = a.v_cur ? a.v_cur[i] : w;
+    s = fma(c, w, s);
+  }
+  const double mine = block_sum(s, red);
+  finalize_partials(mine, a.partial, a.counter, a.out, a.v_cur == nullptr, red);
+}
+
+// ---- v = w / *h ----
+__global__ void scale_div_kernel(long long n, const double* w, const double* h, double* v) {
+  const double d = *h;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = w[i] / d;
+}
+
+// ---- sum of a per-CTA partial vector on device (power iteration norm) ----
+__global__ void reduce_partials_kernel(const double* partial, int m, double* out, int sqrt_out) {
+  __shared__ double red[TPB];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < m; b += blockDim.x) s += partial[b];
+  const double tot = block_sum(s, red);
+  if (threadIdx.x == 0) *out = sqrt_out ? sqrt(tot) : tot;
+}
+
+// ---- v = w * (1 / *nrm) variant used by power iteration: v = w / est ----
+// (identical to scale_div_kernel; kept as one entry point)
+
+// ---- sum_i y_i v_i over a device pointer table (GMRES final update, krylov.py:89-93) ----
+__global__ void lincomb_kernel(long long n, int k, const double* const* vs, const double* y,
+                               double* z) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s = s + y[j] * vs[j][i];
+    z[i] = s;
+  }
+}
+
+// ---- separable fields: out = coef * (g[x]*g[y])*g[z] ----
+__global__ void outer3_kernel(const __grid_constant__ SpkSepArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.g.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x, y, z;
+    decompose(i, a.g, x, y, z);
+    const double gx = a.g.Ex ? a.gx[x] : 1.0;
+    const double gy = a.g.Ey ? a.gx[y] : 1.0;
+    a.out[i] = (gx * gy) * a.gx[z];
+  }
+}
+
+// ---- stage RHS (SPEC irk_solver.assemble_rhs, sign per test_fem.py:268-274):
+//      w_j = T_j * Fhat - Ku ;  rhs_i = mask * sum_j Ainv_ij w_j
+__global__ void rhs_kernel(const __grid_constant__ SpkRhsArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.g.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x, y, z;
+    decompose(i, a.g, x, y, z);
+    const double gx = a.g.Ex ? a.gx[x] : 1.0;
+    const double gy = a.g.Ey ? a.gx[y] : 1.0;
+    const double fhat = (gx * gy) * a.gx[z];
+    const double ku = a.ku[i];
+    const bool bnd = bnd3(a.g, x, y, z);
+    double w[SPK_CMAX];
+#pragma unroll
+    for (int j = 0; j < SPK_CMAX; ++j)
+      if (j < a.Q) w[j] = a.T[j] * fhat - ku;
+    for (int q = 0; q < a.Q; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < SPK_CMAX; ++j)
+        if (j < a.Q) s = s + a.Ainv[q * SPK_CMAX + j] * w[j];
+      a.out[(long long)q * a.g.n + i] = bnd ? 0.0 : s;
+    }
+  }
+}
+
+// ---- u_{n+1} = u_n + tau * sum_i b_i k_i ----
+__global__ void update_kernel(long long n, int Q, const double* k, const double* bw, double tau,
+                              double* u) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < Q; ++q) s = s + bw[q] * k[(long long)q * n + i];
+    u[i] = u[i] + tau * s;
+  }
+}
+
+__global__ void mask_kernel(long long total, SpkDims g, double* u, double value) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x, y, z;
+    decompose(i % g.n, g, x, y, z);
+    if (bnd3(g, x, y, z)) u[i] = value;
+  }
+}
+
+int grid_for(long long n) {
+  long long b = (n + TPB - 1) / TPB;
+  const long long cap = 148LL * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s) {
+  const long long total = (long long)a.nblk * a.g.n;
+  const int nb = grid_for(total);
+  switch (K) {
+    case 1: cheb_init_kernel<1><<<nb, TPB, 0, s>>>(a); break;
+    case 2: cheb_init_kernel<2><<<nb, TPB, 0, s>>>(a); break;
+    case 3: cheb_init_kernel<3><<<nb, TPB, 0, s>>>(a); break;
+    case 4: cheb_init_kernel<4><<<nb, TPB, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s) {
+  axpy_flag_kernel<<<grid_for(total), TPB, 0, s>>>(total, x, d, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s) {
+  const long long total = a.outer * (long long)a.nout * a.inner;
+  const int nb = grid_for(total);
+  switch (K) {
+    case 1: transfer_axis_kernel<1><<<nb, TPB, 0, s>>>(a); break;
+    case 2: transfer_axis_kernel<2><<<nb, TPB, 0, s>>>(a); break;
+    case 3: transfer_axis_kernel<3><<<nb, TPB, 0, s>>>(a); break;
+    case 4: transfer_axis_kernel<4><<<nb, TPB, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s) {
+  combine_kernel<<<grid_for(a.n), TPB, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int spk_mgs_grid() { return 148 * 2; }
+
+cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s) {
+  mgs_kernel<<<spk_mgs_grid(), TPB, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s) {
+  scale_div_kernel<<<grid_for(n), TPB, 0, s>>>(n, w, h, v);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s) {
+  reduce_partials_kernel<<<1, TPB, 0, s>>>(partial, m, out, sqrt_out);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_lincomb(long long n, int k, const double* const* vs, const double* y, double* z,
+                               cudaStream_t s) {
+  lincomb_kernel<<<grid_for(n), TPB, 0, s>>>(n, k, vs, y, z);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_outer3(const SpkSepArgs& a, cudaStream_t s) {
+  outer3_kernel<<<grid_for(a.g.n), TPB, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_rhs(const SpkRhsArgs& a, cudaStream_t s) {
+  rhs_kernel<<<grid_for(a.g.n), TPB, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_update(long long n, int Q, const double* k, const double* bw, double tau, double* u,
+                              cudaStream_t s) {
+  update_kernel<<<grid_for(n), TPB, 0, s>>>(n, Q, k, bw, tau, u);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_mask(long long total, const SpkDims& g, double* u, double value, cudaStream_t s) {
+  mask_kernel<<<grid_for(total), TPB, 0, s>>>(total, g, u, value);
+  return cudaGetLastError();
+}
