@@ -18,7 +18,7 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_spk.so")
+LIB_PATH = os.environ.get("SPK_LIB_PATH", os.path.join(_HERE, "_spk.so"))
 
 c_int = ctypes.c_int
 c_ll = ctypes.c_longlong

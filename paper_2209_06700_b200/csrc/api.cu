@@ -155,11 +155,27 @@ SpkApplyArgs base_args(const spk_ctx* c, int level) {
   a.g = c->dims[level];
   a.t = c->tabs[level];
   a.store_last = 1;
+  a.hd = std::pow(c->h[level], c->dim);
+  a.hk = std::pow(c->h[level], c->dim - 2);
   return a;
 }
 
-int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a, cudaStream_t s,
+int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a0, cudaStream_t s,
                  int* nctas = nullptr) {
+  // the kernels work with reference-element tables: M = h^d M_hat, K = h^(d-2) K_hat
+  SpkApplyArgs a = a0;
+  bool ident = !block_mode;
+  for (int i = 0; i < SPK_QMAX; ++i)
+    for (int j = 0; j < SPK_QMAX; ++j) {
+      if (i < Q && j < Q && i != j && a0.DM[i][j] != 0.0) ident = false;
+      a.DM[i][j] *= a0.hd;
+      a.DK[i][j] *= a0.hk;
+    }
+  a.dm_identity = ident ? 1 : 0;  // D_M diagonal (e.g. I (x) M): Q fewer FMAs per stage-DoF
+  for (int i = 0; i < SPK_BMAX; ++i) a.lam[i] *= a0.hd;
+  a.tau *= a0.hk;
+  a.jre *= a0.hd;
+  a.jim *= a0.hd;
   cudaError_t e = spk_launch_apply(c->K, Q, block_mode, epi, a, s, nctas);
   if (e != cudaSuccess) return cuda_fail(e, "stage_apply launch");
   return SPK_OK;

@@ -47,6 +47,7 @@ struct SpkApplyArgs {
   // coupled mode: v_i = sum_j DM_ij M u_j + DK_ij K u_j
   double DM[SPK_QMAX][SPK_QMAX];
   double DK[SPK_QMAX][SPK_QMAX];
+  int dm_identity;        // coupled mode: DM is the identity (scaled by h^d) -> cheaper mix
   // block mode: v_b = lam_b M u_b + tau K u_b   (lam_uniform: lam[0] for every block)
   double lam[SPK_BMAX];
   int lam_uniform;
@@ -62,6 +63,7 @@ struct SpkApplyArgs {
   // Jacobi diagonal: block mode diag = lam_b*dm + tau*dk ; pair mode uses (re, im, tau)
   double jre, jim;
   double* partial;        // EPI_DINV: per-CTA partial sums (deterministic reduction)
+  double hd, hk;          // host only: h^dim and h^(dim-2) folded into the mix by the launcher
 };
 
 // launchers (stage_apply.cu)

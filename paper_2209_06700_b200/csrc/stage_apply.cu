@@ -6,17 +6,21 @@
 // M = Mx(x)My(x)Mz and K = Kx My Mz + Mx Ky Mz + Mx My Kz are the Kronecker forms the reference
 // applies with dense 1D contractions (fem.py:120-151, _contract fem.py:37-41). Here the assembled
 // 1D matrices are never formed: each axis is applied element-by-element from the (k+1)x(k+1)
-// element tables, which gives the flop-minimal banded form (SURVEY.md §7 hard part 1).
+// reference-element tables (compile-time constants, spk_tables.cuh), which is the flop-minimal
+// banded form (SURVEY.md §7 hard part 1). The mesh size is folded into the stage mix:
+// M = h^d M_hat, K = h^(d-2) K_hat, so the host passes DM' = h^d DM and DK' = h^(d-2) DK.
 //
 // Schedule ("2.5D sliding window", one CTA = one (y,z) tile x one x-chunk, all Q stages):
 //   per x-plane:  cp.async plane x+1 into the other smem buffer (double buffering)
-//                 Z-phase   a = Mz u, b = Kz u                 (smem -> smem, register-blocked)
-//                 Y-phase   ma = My a, c = Ky a + My b          (smem -> smem)
+//                 Z-phase   a = Mz u, b = Kz u                 (smem -> smem, 2 elements / item)
+//                 Y-phase   ma = My a, c = Ky a + My b          (smem -> smem, 2 elements / item)
 //                 X-phase   stage mix p_i = sum_j DM_ij ma_j + DK_ij c_j, q_i = sum_j DK_ij ma_j
 //                           and element-push accumulation v += Mx[.,r] p + Kx[.,r] q in registers
 //   an element's K output planes are finished when its last plane arrives -> fused epilogue.
+// Every thread's work items are fixed for the whole kernel (no per-plane index arithmetic).
 // HBM traffic per apply: read u once (+ L2-resident halo), write v once = 16 B per stage-DoF.
 #include "spk_internal.cuh"
+#include "spk_tables.cuh"
 
 namespace {
 
@@ -29,14 +33,77 @@ template <> struct Tile<4> { static constexpr int TYE = 4, TZE = 8; };
 template <int K, int Q> struct Geo {
   static constexpr int TYE = Tile<K>::TYE, TZE = Tile<K>::TZE;
   static constexpr int TY = K * TYE, TZ = K * TZE;
+  // 1 barrier per plane: Z, Y, X run on three plane buffers (see the pipeline below)
+  static constexpr bool PIPE3 = true;
+  static constexpr int NT = (Q >= 2) ? 512 : 256;
+  static constexpr int NBUF = PIPE3 ? 2 : 1;
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
   static constexpr int TZp = TZ | 1;
   static constexpr int U_SZ = Q * NYin * NZp;          // one plane buffer
-  static constexpr int AB_SZ = Q * NYin * TZp;
-  static constexpr int MC_SZ = Q * TY * TZp;
-  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * AB_SZ + 2 * MC_SZ;
-  static constexpr int PPT = (TY * TZ + SPK_THREADS - 1) / SPK_THREADS;
+  static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
+  static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ;
+  static constexpr int PPT = (TY * TZ + NT - 1) / NT;
+  // Z items: (q, yy, element segment), ZS elements per segment
+  static constexpr int ZS = (Q >= 2) ? 2 : 1;
+  static constexpr int ZSEG = (TZE + ZS - 1) / ZS;
+  static constexpr int ZITEMS = Q * NYin * ZSEG;
+  static constexpr int ZIT = (ZITEMS + NT - 1) / NT;
+  // Y items: (q, z, element segment)
+  static constexpr int YS = 1;
+  static constexpr int YSEG = (TYE + YS - 1) / YS;
+  static constexpr int YITEMS = Q * TZ * YSEG;
+  static constexpr int YIT = (YITEMS + NT - 1) / NT;
+  // U load items
+  static constexpr int LITEMS = Q * NYin * NZin;
+  static constexpr int LIT = (LITEMS + NT - 1) / NT;
+  static constexpr int MINB = (!PIPE3 && SMEM_DOUBLES * 8 <= 113 * 1024) ? 2 : 1;
+};
+
+// Distinct entries of a symmetric, centro-symmetric (K+1)x(K+1) element table:
+// (r,s) ~ (s,r) ~ (K-r,K-s) ~ (K-s,K-r). cls() maps an entry to its class, NC classes in total.
+template <int K> struct Sym {
+  __host__ __device__ static constexpr int canon(int r, int s) {
+    int best = r * 16 + s;
+    const int c2 = s * 16 + r, c3 = (K - r) * 16 + (K - s), c4 = (K - s) * 16 + (K - r);
+    if (c2 < best) best = c2;
+    if (c3 < best) best = c3;
+    if (c4 < best) best = c4;
+    return best;
+  }
+  __host__ __device__ static constexpr int cls(int r, int s) {
+    const int me = canon(r, s);
+    int n = 0;
+    for (int a = 0; a <= K; ++a)
+      for (int b = 0; b <= K; ++b)
+        if (canon(a, b) == a * 16 + b && a * 16 + b < me) ++n;
+    return n;
+  }
+  __host__ __device__ static constexpr int count() {
+    int n = 0;
+    for (int a = 0; a <= K; ++a)
+      for (int b = 0; b <= K; ++b)
+        if (canon(a, b) == a * 16 + b) ++n;
+    return n;
+  }
+};
+
+// reference-element mass (M) and stiffness (S) tables held in registers
+template <int K> struct Coef {
+  static constexpr int NC = Sym<K>::count();
+  double mv[NC], sv[NC];
+  __device__ __forceinline__ void load() {
+#pragma unroll
+    for (int r = 0; r <= K; ++r)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) {
+        mv[Sym<K>::cls(r, s)] = c_hat[K - 1][0][r][s];
+        sv[Sym<K>::cls(r, s)] = c_hat[K - 1][1][r][s];
+      }
+  }
+  __device__ __forceinline__ double m(int r, int s) const { return mv[Sym<K>::cls(r, s)]; }
+  __device__ __forceinline__ double s(int r, int s2) const { return sv[Sym<K>::cls(r, s2)]; }
 };
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
@@ -47,26 +114,33 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// assembled 1D diagonal at node i of an axis with E elements (E == 0: degenerate axis)
+// assembled 1D reference diagonal at node i of an axis with E elements (E == 0: degenerate axis)
 template <int K>
-__device__ __forceinline__ void diag1(const SpkTab& t, int i, int E, double& dm, double& dk) {
+__device__ __forceinline__ void diag1(int i, int E, double& dm, double& dk) {
+  using H = Hat<K>;
   if (E == 0) { dm = 1.0; dk = 0.0; return; }
   const int e = i / K, r = i - e * K;
-  if (r != 0) { dm = t.Me[r][r]; dk = t.Ke[r][r]; return; }
+  if (r != 0) {
+    double m = 0.0, s = 0.0;
+#pragma unroll
+    for (int rr = 1; rr < K; ++rr)
+      if (rr == r) { m = H::M(rr, rr); s = H::S(rr, rr); }
+    dm = m; dk = s;
+    return;
+  }
   dm = 0.0; dk = 0.0;
-  if (e > 0) { dm += t.Me[K][K]; dk += t.Ke[K][K]; }
-  if (e < E) { dm += t.Me[0][0]; dk += t.Ke[0][0]; }
+  if (e > 0) { dm += H::M(K, K); dk += H::S(K, K); }
+  if (e < E) { dm += H::M(0, 0); dk += H::S(0, 0); }
 }
 
-// diag(lam M + tau K) pieces at a node, same association order as the reference's
-// np.multiply.outer chain (fem.py:172-187)
+// reference-element diagonal pieces at a node (association order of np.multiply.outer chains,
+// reference fem.py:172-187); the caller scales by DM' / DK'
 template <int K>
-__device__ __forceinline__ void node_diag(const SpkTab& t, const SpkDims& g, int x, int y, int z,
-                                          double& dm, double& dk) {
+__device__ __forceinline__ void node_diag(const SpkDims& g, int x, int y, int z, double& dm, double& dk) {
   double mx, kx, my, ky, mz, kz;
-  diag1<K>(t, x, g.Ex, mx, kx);
-  diag1<K>(t, y, g.Ey, my, ky);
-  diag1<K>(t, z, g.Ez, mz, kz);
+  diag1<K>(x, g.Ex, mx, kx);
+  diag1<K>(y, g.Ey, my, ky);
+  diag1<K>(z, g.Ez, mz, kz);
   dm = (mx * my) * mz;
   dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
 }
@@ -76,62 +150,60 @@ __device__ __forceinline__ bool on_boundary(const SpkDims& g, int x, int y, int 
          (g.Ez > 0 && (z == 0 || z == g.nz - 1));
 }
 
-// One element-wise 1D application of two tables on the same input:
-//   vertex r=0 gathers the left element (row K) and the right element (row 0);
-//   interior r>=1 use the right element only.
+// z-sweep of one element: vertex r=0 gathers the left element (row K) and the right element
+// (row 0); interior r>=1 use the right element only. Outputs a = M_hat u, b = K_hat u.
 template <int K>
-__device__ __forceinline__ void elem2(const double (&L)[K + 1], const double (&R)[K + 1], double wl,
-                                      double wr, const double (&E1)[SPK_KMAX + 1][SPK_KMAX + 1],
-                                      const double (&E2)[SPK_KMAX + 1][SPK_KMAX + 1], double (&o1)[K],
-                                      double (&o2)[K]) {
+__device__ __forceinline__ void elem2(const Coef<K>& cf, const double (&L)[K + 1], const double (&R)[K + 1],
+                                      double wl, double wr, double (&o1)[K], double (&o2)[K]) {
   double l1 = 0.0, l2 = 0.0, r1 = 0.0, r2 = 0.0;
 #pragma unroll
   for (int s = 0; s <= K; ++s) {
-    l1 = fma(E1[K][s], L[s], l1);
-    l2 = fma(E2[K][s], L[s], l2);
-    r1 = fma(E1[0][s], R[s], r1);
-    r2 = fma(E2[0][s], R[s], r2);
+    l1 = fma(cf.m(K, s), L[s], l1);
+    l2 = fma(cf.s(K, s), L[s], l2);
+    r1 = fma(cf.m(0, s), R[s], r1);
+    r2 = fma(cf.s(0, s), R[s], r2);
   }
-  o1[0] = wl * l1 + wr * r1;
-  o2[0] = wl * l2 + wr * r2;
+  o1[0] = fma(wl, l1, wr * r1);
+  o2[0] = fma(wl, l2, wr * r2);
 #pragma unroll
   for (int r = 1; r < K; ++r) {
     double a1 = 0.0, a2 = 0.0;
 #pragma unroll
     for (int s = 0; s <= K; ++s) {
-      a1 = fma(E1[r][s], R[s], a1);
-      a2 = fma(E2[r][s], R[s], a2);
+      a1 = fma(cf.m(r, s), R[s], a1);
+      a2 = fma(cf.s(r, s), R[s], a2);
     }
     o1[r] = a1;
     o2[r] = a2;
   }
 }
 
-// y-sweep on two inputs: ma = M a ; c = K a + M b
+// y-sweep of one element on two inputs: ma = M_hat a ; c = K_hat a + M_hat b
 template <int K>
-__device__ __forceinline__ void elem3(const double (&La)[K + 1], const double (&Ra)[K + 1],
-                                      const double (&Lb)[K + 1], const double (&Rb)[K + 1], double wl,
-                                      double wr, const SpkTab& t, double (&ma)[K], double (&c)[K]) {
+__device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 1],
+                                      const double (&Ra)[K + 1], const double (&Lb)[K + 1],
+                                      const double (&Rb)[K + 1], double wl, double wr, double (&ma)[K],
+                                      double (&c)[K]) {
   double lm = 0.0, lc = 0.0, rm = 0.0, rc = 0.0;
 #pragma unroll
   for (int s = 0; s <= K; ++s) {
-    lm = fma(t.Me[K][s], La[s], lm);
-    lc = fma(t.Ke[K][s], La[s], lc);
-    lc = fma(t.Me[K][s], Lb[s], lc);
-    rm = fma(t.Me[0][s], Ra[s], rm);
-    rc = fma(t.Ke[0][s], Ra[s], rc);
-    rc = fma(t.Me[0][s], Rb[s], rc);
+    lm = fma(cf.m(K, s), La[s], lm);
+    lc = fma(cf.s(K, s), La[s], lc);
+    lc = fma(cf.m(K, s), Lb[s], lc);
+    rm = fma(cf.m(0, s), Ra[s], rm);
+    rc = fma(cf.s(0, s), Ra[s], rc);
+    rc = fma(cf.m(0, s), Rb[s], rc);
   }
-  ma[0] = wl * lm + wr * rm;
-  c[0] = wl * lc + wr * rc;
+  ma[0] = fma(wl, lm, wr * rm);
+  c[0] = fma(wl, lc, wr * rc);
 #pragma unroll
   for (int r = 1; r < K; ++r) {
     double am = 0.0, ac = 0.0;
 #pragma unroll
     for (int s = 0; s <= K; ++s) {
-      am = fma(t.Me[r][s], Ra[s], am);
-      ac = fma(t.Ke[r][s], Ra[s], ac);
-      ac = fma(t.Me[r][s], Rb[s], ac);
+      am = fma(cf.m(r, s), Ra[s], am);
+      ac = fma(cf.s(r, s), Ra[s], ac);
+      ac = fma(cf.m(r, s), Rb[s], ac);
     }
     ma[r] = am;
     c[r] = ac;
@@ -139,7 +211,7 @@ __device__ __forceinline__ void elem3(const double (&La)[K + 1], const double (&
 }
 
 template <int K, int Q, bool BLOCK, int EPI>
-__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, int x, int y, int z,
+__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, double lamb, int x, int y, int z,
                                          const double (&val)[Q], double& sumsq) {
   const SpkDims& g = a.g;
   const long long gi = ((long long)x * g.ny + y) * g.nz + z;
@@ -154,15 +226,14 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, int x, 
   if constexpr (EPI == EPI_STORE) {
     const long long vbase = BLOCK ? (long long)blk * a.sv : 0;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) a.v[vbase + q * a.sv + gi] = Av[q];
+    for (int q = 0; q < Q; ++q) __stcs(a.v + vbase + q * a.sv + gi, Av[q]);
   } else {
     // Jacobi diagonal (analytic; reference operator_diagonal fem.py:172-187, 1.0 on boundary)
     double dm, dk;
-    node_diag<K>(a.t, g, x, y, z, dm, dk);
+    node_diag<K>(g, x, y, z, dm, dk);
     if constexpr (EPI == EPI_DINV) {
       if constexpr (BLOCK || Q == 1) {
-        const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
-        const double inv = bnd ? 1.0 : 1.0 / (lam * dm + a.tau * dk);
+        const double inv = bnd ? 1.0 : 1.0 / (lamb * dm + a.tau * dk);
         const double w = inv * Av[0];
         const long long vbase = BLOCK ? (long long)blk * a.sv : 0;
         a.v[vbase + gi] = w;
@@ -200,8 +271,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, int x, 
         const double c2 = a.c2[slot];
         double z0[Q];
         if constexpr (BLOCK || Q == 1) {
-          const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
-          const double inv = bnd ? 1.0 : 1.0 / (lam * dm + a.tau * dk);
+          const double inv = bnd ? 1.0 : 1.0 / (lamb * dm + a.tau * dk);
           z0[0] = inv * rn[0];
         } else {
           const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
@@ -228,19 +298,17 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int blk, int x, 
 }
 
 template <int K, int Q, bool BLOCK, int EPI>
-__global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
+__global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
     stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
   using G = Geo<K, Q>;
-  constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ;
+  constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;
   constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
   constexpr int PPT = G::PPT;
 
   extern __shared__ double smem[];
   double* Us = smem;                    // [2][Q][NYin][NZp]
-  double* As = Us + 2 * G::U_SZ;        // [Q][NYin][TZp]
-  double* Bs = As + G::AB_SZ;
-  double* MAs = Bs + G::AB_SZ;          // [Q][TY][TZp]
-  double* Cs = MAs + G::MC_SZ;
+  double* ABs = Us + 2 * G::U_SZ;       // [2][A|B][Q][NYin][TZp]
+  double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][MA|C][Q][TY][TZp]
 
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
@@ -256,9 +324,12 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
   const int ney = ydeg ? 1 : min(TYE, g.Ey + 1 - ey0);
   const double* __restrict__ u = a.u + (BLOCK ? (long long)blk * a.su : 0);
 
-  // block mode coefficients
   double lamb = 0.0;
   if constexpr (BLOCK) lamb = a.lam_uniform ? a.lam[0] : a.lam[blk - a.blk_base];
+
+  // reference-element tables in registers (distinct entries only)
+  Coef<K> cf;
+  cf.load();
 
   // x-chunk (elements [ex0, ex1)); planes K*(ex0-1) .. K*ex1
   int ex0 = 0, ex1 = 0, xs = 0, nplanes = 1, ecur = 0;
@@ -270,32 +341,179 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
     nplanes = K * ex1 - xs + 1;
   }
 
-  const int yy_lo = ydeg ? K : 0, yy_hi = ydeg ? K + 1 : NYin;
-
-  auto load_plane = [&](int x, int buf) {
-    double* dst = Us + buf * G::U_SZ;
-    const long long xoff = (long long)x * g.ny;
-    const bool xb = a.constrained && !xdeg && (x == 0 || x == g.nx - 1);
-    for (int idx = tid; idx < Q * NYin * NZin; idx += SPK_THREADS) {
+  // ---- fixed per-thread work descriptors ----
+  const long long plane_stride = (long long)g.ny * g.nz;
+  const double* lsrc[G::LIT];
+  unsigned ldst[G::LIT];
+  bool lbnd[G::LIT];
+#pragma unroll
+  for (int i = 0; i < G::LIT; ++i) {
+    const int idx = tid + i * NT;
+    lsrc[i] = nullptr;
+    ldst[i] = 0xffffffffu;
+    lbnd[i] = false;
+    if (idx < G::LITEMS) {
       const int q = idx / (NYin * NZin);
       const int rem = idx - q * (NYin * NZin);
       const int yy = rem / NZin, zz = rem - yy * NZin;
       const int gy = y_lo - K + yy, gz = z_lo - K + zz;
-      bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
-      if (in && a.constrained)
-        in = !(xb || (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1);
-      const double* src = in ? u + (long long)q * a.su + (xoff + gy) * g.nz + gz : u;
-      cp_async8(dst + (q * NYin + yy) * NZp + zz, src, in ? 8 : 0);
+      ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + (q * NYin + yy) * NZp + zz));
+      if (gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz) {
+        lsrc[i] = u + (long long)q * a.su + (long long)gy * g.nz + gz;
+        lbnd[i] = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
+      }
+    }
+  }
+  constexpr unsigned UBUF = G::U_SZ * sizeof(double);
+
+  auto load_plane = [&](int x, int buf) {
+    const bool xb = !xdeg && (x == 0 || x == g.nx - 1);
+    const long long xoff = (long long)x * plane_stride;
+#pragma unroll
+    for (int i = 0; i < G::LIT; ++i) {
+      if (ldst[i] == 0xffffffffu) continue;
+      bool in = lsrc[i] != nullptr;
+      if (a.constrained) in = in && !(xb || lbnd[i]);
+      const double* src = in ? lsrc[i] + xoff : u;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
+                   "l"(src), "r"(in ? 8 : 0) : "memory");
     }
     cp_async_commit();
   };
 
-  // Z/Y work partition: segments of consecutive elements per item so loads are reused
-  const int zrows = yy_hi - yy_lo;
-  const int nsegz = max(1, min(nez, SPK_THREADS / (Q * zrows)));
-  const int lenz = (nez + nsegz - 1) / nsegz;
-  const int nsegy = ydeg ? 1 : max(1, min(ney, SPK_THREADS / (Q * max(nzo, 1))));
-  const int leny = (ney + nsegy - 1) / nsegy;
+  // Z items: (q, yy, segment of ZS elements); lanes run along yy (odd pitch -> no bank conflicts)
+  int zoff[G::ZIT], zeb[G::ZIT];
+#pragma unroll
+  for (int i = 0; i < G::ZIT; ++i) {
+    const int it = tid + i * NT;
+    zeb[i] = TZE;  // inactive
+    zoff[i] = 0;
+    if (it < G::ZITEMS) {
+      const int yy = it % NYin;
+      const int rest = it / NYin;
+      const int seg = rest % G::ZSEG, q = rest / G::ZSEG;
+      if (!ydeg || yy == K) {
+        zeb[i] = seg * G::ZS;
+        zoff[i] = q * NYin + yy;  // row index
+      }
+    }
+  }
+  // Y items: (q, z, segment of YS elements); lanes run along z
+  int yoff[G::YIT], yeb[G::YIT];
+#pragma unroll
+  for (int i = 0; i < G::YIT; ++i) {
+    const int it = tid + i * NT;
+    yeb[i] = TYE;
+    yoff[i] = 0;
+    if (it < G::YITEMS) {
+      const int zl = it % TZ;
+      const int rest = it / TZ;
+      const int seg = rest % G::YSEG, q = rest / G::YSEG;
+      if (zl < nzo) {
+        yeb[i] = seg * G::YS;
+        yoff[i] = q * 4096 + zl;  // packed (q, zl)
+      }
+    }
+  }
+
+  // ---------------- Z-phase: A = Mz u, B = Kz u ----------------
+  auto zphase = [&](int ub, int ab) {
+    const double* Ub = Us + ub * G::U_SZ;
+    double* As = ABs + ab * 2 * G::AB_SZ;
+    double* Bs = As + G::AB_SZ;
+#pragma unroll
+    for (int i = 0; i < G::ZIT; ++i) {
+      if (zeb[i] >= nez) continue;
+      const double* row = Ub + zoff[i] * NZp;
+      double* arow = As + zoff[i] * TZp;
+      double* brow = Bs + zoff[i] * TZp;
+      const int e_beg = zeb[i];
+      double L[K + 1], R[K + 1];
+#pragma unroll
+      for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
+#pragma unroll
+      for (int el = 0; el < G::ZS; ++el) {
+        const int e = e_beg + el;
+        if (e < nez) {
+          R[0] = L[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) R[s] = row[K * e + K + s];
+          const int ez = ez0 + e;
+          const double wl = ez > 0 ? 1.0 : 0.0, wr = ez < g.Ez ? 1.0 : 0.0;
+          double oa[K], ob[K];
+          elem2<K>(cf, L, R, wl, wr, oa, ob);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int zl = K * e + r;
+            if (r == 0 || zl < nzo) { arow[zl] = oa[r]; brow[zl] = ob[r]; }
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) L[s] = R[s];
+        }
+      }
+    }
+  };
+
+  // ---------------- Y-phase: MA = My A, C = Ky A + My B ----------------
+  auto yphase = [&](int ab, int mc) {
+    const double* As = ABs + ab * 2 * G::AB_SZ;
+    const double* Bs = As + G::AB_SZ;
+    double* MAs = MCs + mc * 2 * G::MC_SZ;
+    double* Cs = MAs + G::MC_SZ;
+    if (ydeg) {
+      for (int it = tid; it < Q * TZ; it += NT) {
+        const int q = it / TZ, zl = it - q * TZ;
+        if (zl < nzo) {
+          MAs[(q * TY) * TZp + zl] = As[(q * NYin + K) * TZp + zl];
+          Cs[(q * TY) * TZp + zl] = Bs[(q * NYin + K) * TZp + zl];
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < G::YIT; ++i) {
+      if (yeb[i] >= ney) continue;
+      const int q = yoff[i] >> 12, zl = yoff[i] & 4095;
+      const double* acol = As + (q * NYin) * TZp + zl;
+      const double* bcol = Bs + (q * NYin) * TZp + zl;
+      double* mcol = MAs + (q * TY) * TZp + zl;
+      double* ccol = Cs + (q * TY) * TZp + zl;
+      const int e_beg = yeb[i];
+      double La[K + 1], Ra[K + 1], Lb[K + 1], Rb[K + 1];
+#pragma unroll
+      for (int s = 0; s <= K; ++s) {
+        La[s] = acol[(K * e_beg + s) * TZp];
+        Lb[s] = bcol[(K * e_beg + s) * TZp];
+      }
+#pragma unroll
+      for (int el = 0; el < G::YS; ++el) {
+        const int e = e_beg + el;
+        if (e < ney) {
+          Ra[0] = La[K];
+          Rb[0] = Lb[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) {
+            Ra[s] = acol[(K * e + K + s) * TZp];
+            Rb[s] = bcol[(K * e + K + s) * TZp];
+          }
+          const int ey = ey0 + e;
+          const double wl = ey > 0 ? 1.0 : 0.0, wr = ey < g.Ey ? 1.0 : 0.0;
+          double om[K], oc[K];
+          elem3<K>(cf, La, Ra, Lb, Rb, wl, wr, om, oc);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int yl = K * e + r;
+            if (r == 0 || yl < nyo) {
+              mcol[yl * TZp] = om[r];
+              ccol[yl * TZp] = oc[r];
+            }
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
+        }
+      }
+    }
+  };
 
   // X-phase state
   double acc[PPT][Q][K + 1];
@@ -303,7 +521,7 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
   bool pv[PPT];
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const int p = tid + j * SPK_THREADS;
+    const int p = tid + j * NT;
     pyl[j] = p / TZ;
     pzl[j] = p - pyl[j] * TZ;
     pv[j] = (p < TY * TZ) && pyl[j] < nyo && pzl[j] < nzo;
@@ -313,101 +531,19 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
       for (int s = 0; s <= K; ++s) acc[j][q][s] = 0.0;
   }
   double sumsq = 0.0;
+  const bool dm_ident = a.dm_identity != 0;
 
-  load_plane(xs, 0);
-  int buf = 0;
-  for (int pl = 0; pl < nplanes; ++pl) {
-    const int x = xs + pl;
-    cp_async_wait_all();
-    __syncthreads();
-    if (pl + 1 < nplanes) load_plane(x + 1, buf ^ 1);
-
-    // ---------------- Z-phase: a = Mz u, b = Kz u on rows [yy_lo, yy_hi) ----------------
-    {
-      const double* Ub = Us + buf * G::U_SZ;
-      for (int it = tid; it < Q * zrows * nsegz; it += SPK_THREADS) {
-        const int yy = yy_lo + it % zrows;
-        const int rest = it / zrows;
-        const int seg = rest % nsegz, q = rest / nsegz;
-        const int e_beg = seg * lenz, e_end = min(nez, e_beg + lenz);
-        if (e_beg >= e_end) continue;
-        const double* row = Ub + (q * NYin + yy) * NZp;
-        double* arow = As + (q * NYin + yy) * TZp;
-        double* brow = Bs + (q * NYin + yy) * TZp;
-        double L[K + 1], R[K + 1];
-#pragma unroll
-        for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
-        for (int el = e_beg; el < e_end; ++el) {
-          R[0] = L[K];
-#pragma unroll
-          for (int s = 1; s <= K; ++s) R[s] = row[K * el + K + s];
-          const int ez = ez0 + el;
-          const double wl = ez > 0 ? 1.0 : 0.0, wr = ez < g.Ez ? 1.0 : 0.0;
-          double oa[K], ob[K];
-          elem2<K>(L, R, wl, wr, a.t.Me, a.t.Ke, oa, ob);
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            const int zl = K * el + r;
-            if (zl < nzo) { arow[zl] = oa[r]; brow[zl] = ob[r]; }
-          }
-#pragma unroll
-          for (int s = 0; s <= K; ++s) L[s] = R[s];
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---------------- Y-phase: ma = My a, c = Ky a + My b ----------------
-    if (ydeg) {
-      for (int it = tid; it < Q * nzo; it += SPK_THREADS) {
-        const int q = it / nzo, zl = it - q * nzo;
-        MAs[(q * TY) * TZp + zl] = As[(q * NYin + K) * TZp + zl];
-        Cs[(q * TY) * TZp + zl] = Bs[(q * NYin + K) * TZp + zl];
-      }
-    } else {
-      for (int it = tid; it < Q * nzo * nsegy; it += SPK_THREADS) {
-        const int zl = it % nzo;
-        const int rest = it / nzo;
-        const int seg = rest % nsegy, q = rest / nsegy;
-        const int e_beg = seg * leny, e_end = min(ney, e_beg + leny);
-        if (e_beg >= e_end) continue;
-        const double* acol = As + (q * NYin) * TZp + zl;
-        const double* bcol = Bs + (q * NYin) * TZp + zl;
-        double La[K + 1], Ra[K + 1], Lb[K + 1], Rb[K + 1];
-#pragma unroll
-        for (int s = 0; s <= K; ++s) {
-          La[s] = acol[(K * e_beg + s) * TZp];
-          Lb[s] = bcol[(K * e_beg + s) * TZp];
-        }
-        for (int el = e_beg; el < e_end; ++el) {
-          Ra[0] = La[K];
-          Rb[0] = Lb[K];
-#pragma unroll
-          for (int s = 1; s <= K; ++s) {
-            Ra[s] = acol[(K * el + K + s) * TZp];
-            Rb[s] = bcol[(K * el + K + s) * TZp];
-          }
-          const int ey = ey0 + el;
-          const double wl = ey > 0 ? 1.0 : 0.0, wr = ey < g.Ey ? 1.0 : 0.0;
-          double om[K], oc[K];
-          elem3<K>(La, Ra, Lb, Rb, wl, wr, a.t, om, oc);
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            const int yl = K * el + r;
-            if (yl < nyo) {
-              MAs[(q * TY + yl) * TZp + zl] = om[r];
-              Cs[(q * TY + yl) * TZp + zl] = oc[r];
-            }
-          }
-#pragma unroll
-          for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---------------- X-phase: stage mix + element-push accumulation ----------------
+  // ---------------- X-phase: stage mix + element-push accumulation ----------------
+  auto xphase = [&](int x, int mc) {
+    const double* MAs = MCs + mc * 2 * G::MC_SZ;
+    const double* Cs = MAs + G::MC_SZ;
     const int r_loc = xdeg ? 0 : x - K * ecur;   // local plane index within element ecur (0..K)
+    double cmx[K + 1], ckx[K + 1];
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      cmx[s] = c_hat[K - 1][0][s][r_loc];
+      ckx[s] = c_hat[K - 1][1][s][r_loc];
+    }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       if (!pv[j]) continue;
@@ -419,39 +555,45 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
         cc[q] = Cs[(q * TY + yl) * TZp + zl];
       }
       if constexpr (BLOCK) {
-        pq[0] = lamb * ma[0] + a.tau * cc[0];
+        pq[0] = fma(lamb, ma[0], a.tau * cc[0]);
         qq[0] = a.tau * ma[0];
       } else {
+        if (dm_ident) {  // D_M diagonal (the IRK operator I(x)M + tau A(x)K)
 #pragma unroll
-        for (int i = 0; i < Q; ++i) {
-          double p = 0.0, s2 = 0.0;
+          for (int i = 0; i < Q; ++i) {
+            double p = a.DM[i][i] * ma[i], s2 = 0.0;
 #pragma unroll
-          for (int jj = 0; jj < Q; ++jj) {
-            p = fma(a.DM[i][jj], ma[jj], p);
-            p = fma(a.DK[i][jj], cc[jj], p);
-            s2 = fma(a.DK[i][jj], ma[jj], s2);
+            for (int jj = 0; jj < Q; ++jj) {
+              p = fma(a.DK[i][jj], cc[jj], p);
+              s2 = fma(a.DK[i][jj], ma[jj], s2);
+            }
+            pq[i] = p;
+            qq[i] = s2;
           }
-          pq[i] = p;
-          qq[i] = s2;
+        } else {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) {
+            double p = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < Q; ++jj) {
+              p = fma(a.DM[i][jj], ma[jj], p);
+              p = fma(a.DK[i][jj], cc[jj], p);
+              s2 = fma(a.DK[i][jj], ma[jj], s2);
+            }
+            pq[i] = p;
+            qq[i] = s2;
+          }
         }
       }
       const int y = y_lo + yl, z = z_lo + zl;
       if (xdeg) {
-        epilogue<K, Q, BLOCK, EPI>(a, blk, 0, y, z, pq, sumsq);
+        epilogue<K, Q, BLOCK, EPI>(a, blk, lamb, 0, y, z, pq, sumsq);
         continue;
       }
-      // accumulate this plane as local node r_loc of element ecur
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
+      for (int q = 0; q < Q; ++q)
 #pragma unroll
-        for (int rr = 0; rr <= K; ++rr) {
-          if (rr == r_loc) {
-#pragma unroll
-            for (int s = 0; s <= K; ++s)
-              acc[j][q][s] = fma(a.t.Me[s][rr], pq[q], fma(a.t.Ke[s][rr], qq[q], acc[j][q][s]));
-          }
-        }
-      }
+        for (int s = 0; s <= K; ++s) acc[j][q][s] = fma(cmx[s], pq[q], fma(ckx[s], qq[q], acc[j][q][s]));
       if (r_loc == K) {
         // element ecur complete: nodes K*ecur + s, s < K
         if (ecur >= ex0) {
@@ -460,28 +602,58 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
             double val[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
-            epilogue<K, Q, BLOCK, EPI>(a, blk, K * ecur + s, y, z, val, sumsq);
+            epilogue<K, Q, BLOCK, EPI>(a, blk, lamb, K * ecur + s, y, z, val, sumsq);
           }
         }
         if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
           double val[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
-          epilogue<K, Q, BLOCK, EPI>(a, blk, K * g.Ex, y, z, val, sumsq);
+          epilogue<K, Q, BLOCK, EPI>(a, blk, lamb, K * g.Ex, y, z, val, sumsq);
         }
         // carry the shared vertex and start the next element with this plane as its local 0
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const double carry = acc[j][q][K];
 #pragma unroll
-          for (int s = 0; s <= K; ++s)
-            acc[j][q][s] = fma(a.t.Me[s][0], pq[q], a.t.Ke[s][0] * qq[q]);
+          for (int s = 0; s <= K; ++s) acc[j][q][s] = fma(cf.m(s, 0), pq[q], cf.s(s, 0) * qq[q]);
           acc[j][q][0] += carry;
         }
       }
     }
     if (!xdeg && r_loc == K) ++ecur;
-    buf ^= 1;
+  };
+
+  if constexpr (G::PIPE3) {
+    // Three-stage software pipeline, ONE barrier per plane: interval t runs Z(t), Y(t-1), X(t-2)
+    // on disjoint double buffers (U/AB/MC indexed by plane parity) while U(t+1) is in flight.
+    load_plane(xs, 0);
+    for (int t = 0; t < nplanes + 2; ++t) {
+      cp_async_wait_all();
+      __syncthreads();
+      if (t + 1 < nplanes) load_plane(xs + t + 1, (t + 1) & 1);
+      if (t < nplanes) zphase(t & 1, t & 1);
+      if (t >= 1 && t - 1 < nplanes) yphase((t - 1) & 1, (t - 1) & 1);
+      if (t >= 2) xphase(xs + t - 2, t & 1);
+    }
+  } else {
+    // Two barriers per plane: Z(x+1) and X(x) share an interval (U/AB vs MC), Y(x+1) follows.
+    load_plane(xs, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    zphase(0, 0);
+    if (nplanes > 1) load_plane(xs + 1, 1);
+    __syncthreads();
+    yphase(0, 0);
+    for (int pl = 0; pl < nplanes; ++pl) {
+      cp_async_wait_all();
+      __syncthreads();                     // U(x+1) landed; MC(x) ready; AB consumed
+      if (pl + 2 < nplanes) load_plane(xs + pl + 2, pl & 1);
+      if (pl + 1 < nplanes) zphase((pl + 1) & 1, 0);
+      xphase(xs + pl, 0);
+      __syncthreads();                     // AB(x+1) ready; MC(x) consumed
+      if (pl + 1 < nplanes) yphase(0, 0);
+    }
   }
 
   if constexpr (EPI == EPI_DINV) {
@@ -490,7 +662,7 @@ __global__ void __launch_bounds__(SPK_THREADS, (Q >= 4 ? 1 : 2))
     double* red = smem;
     red[tid] = sumsq;
     __syncthreads();
-    for (int off = SPK_THREADS / 2; off > 0; off >>= 1) {
+    for (int off = NT / 2; off > 0; off >>= 1) {
       if (tid < off) red[tid] += red[tid + off];
       __syncthreads();
     }
@@ -517,7 +689,7 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
   const int nb = BLOCK ? a.nblk : 1;
   dim3 grid(gz, gy, a.nchunks * nb);
   if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
-  kern<<<grid, SPK_THREADS, smem, s>>>(a);
+  kern<<<grid, G::NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -564,6 +736,18 @@ cudaError_t spk_launch_apply(int K, int Q, bool block_mode, int epi, const SpkAp
 int spk_apply_smem_bytes(int K, int Q) {
   switch (K * 16 + Q) {
 #define SPK_CASE(k, q) case k * 16 + q: return (int)(sizeof(double) * Geo<k, q>::SMEM_DOUBLES);
+    SPK_CASE(1, 1) SPK_CASE(1, 2) SPK_CASE(1, 3) SPK_CASE(1, 4)
+    SPK_CASE(2, 1) SPK_CASE(2, 2) SPK_CASE(2, 3) SPK_CASE(2, 4)
+    SPK_CASE(3, 1) SPK_CASE(3, 2) SPK_CASE(3, 3) SPK_CASE(3, 4)
+    SPK_CASE(4, 1) SPK_CASE(4, 2) SPK_CASE(4, 3) SPK_CASE(4, 4)
+#undef SPK_CASE
+  }
+  return -1;
+}
+
+int spk_apply_threads(int K, int Q) {
+  switch (K * 16 + Q) {
+#define SPK_CASE(k, q) case k * 16 + q: return Geo<k, q>::NT;
     SPK_CASE(1, 1) SPK_CASE(1, 2) SPK_CASE(1, 3) SPK_CASE(1, 4)
     SPK_CASE(2, 1) SPK_CASE(2, 2) SPK_CASE(2, 3) SPK_CASE(2, 4)
     SPK_CASE(3, 1) SPK_CASE(3, 2) SPK_CASE(3, 3) SPK_CASE(3, 4)
