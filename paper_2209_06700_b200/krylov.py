@@ -1,0 +1,245 @@
+"""Right-preconditioned GMRES (modified Gram-Schmidt, no restart) on device vectors.
+
+Same contract as the reference krylov.gmres (krylov.py:28-103): signature, KrylovReport fields,
+stopping rule (lstsq residual <= rel_tol * beta), happy breakdown below 1e-30, final x =
+P^{-1}(sum_i y_i v_i), true residual recomputed, NumericalFailureError on non-finite values.
+
+The Krylov basis lives in HBM; every MGS step is one fused sweep (spk_mgs: w -= h_prev v_prev and
+the next dot, deterministic two-level reduction) whose result stays in a device Hessenberg array,
+so an iteration costs j+2 memory-bound launches and ONE device->host copy (the new Hessenberg column
+for the host least-squares solve, done with numpy like the reference, krylov.py:106-110).
+
+Host (numpy) right-hand sides and callables are accepted for drop-in use: the vectors still live on
+the device and the callables are bridged. Complex fields use the real (re, im) interleaved view with
+the complex inner product computed on device.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import ptr, require_cuda, stream_ptr
+from .errors import NumericalFailureError
+
+BREAKDOWN_TOL = 1e-30
+
+
+@dataclass
+class KrylovReport:
+    """Convergence record of one GMRES solve."""
+
+    iterations: int = 0
+    residual_history: list = field(default_factory=list)
+    converged: bool = False
+    reduction_achieved: float = 1.0
+
+
+_NULL_CTX = None
+
+
+def _ctx():
+    global _NULL_CTX
+    if _NULL_CTX is None:
+        c = _lib.c_vp()
+        _lib.check(_lib.load().spk_ctx_create(1, 1, 1, _lib.ctypes.byref(c)))
+        _NULL_CTX = c
+    return _NULL_CTX
+
+
+def _solve_hessenberg(Hk, gk):
+    y, *_ = np.linalg.lstsq(Hk, gk, rcond=None)
+    res = float(np.linalg.norm(gk - Hk @ y))
+    return y, res
+
+
+class _Bridge:
+    """Adapts user callables to device tensors of one fixed shape/dtype."""
+
+    def __init__(self, fn, shape, host, complex_, device):
+        self.fn, self.shape, self.host, self.complex, self.device = fn, shape, host, complex_, device
+
+    def to_user(self, v):
+        x = v.reshape(self.shape + ((2,) if self.complex else ()))
+        if self.complex:
+            x = torch.view_as_complex(x)
+        return x.cpu().numpy() if self.host else x
+
+    def from_user(self, y):
+        if self.host:
+            arr = np.asarray(y)
+            t = torch.from_numpy(np.ascontiguousarray(arr.astype(np.complex128 if self.complex else np.float64)))
+            t = t.to(self.device)
+        else:
+            t = y if isinstance(y, torch.Tensor) else torch.as_tensor(y, device=self.device)
+            t = t.to(torch.complex128 if self.complex else torch.float64)
+        if self.complex:
+            t = torch.view_as_real(t.contiguous())
+        return t.contiguous().reshape(-1)
+
+    def __call__(self, v):
+        if self.fn is None:
+            return v
+        return self.from_user(self.fn(self.to_user(v)))
+
+
+class _Ops:
+    """Device inner products / updates for real vectors or complex vectors in (re, im) view."""
+
+    def __init__(self, n, complex_, device, max_iter):
+        self.n, self.complex, self.device = n, complex_, device
+        self.st = stream_ptr(device)
+        self.ctx = _ctx()
+        # Hessenberg columns: col j holds H[0..j+1, j]; complex: (re, im) pairs
+        w = 2 if complex_ else 1
+        self.H = torch.zeros((max_iter + 2) * (max_iter + 2) * w, dtype=torch.float64, device=device)
+        self.scal = torch.zeros(8, dtype=torch.float64, device=device)
+        self.scal[0] = 1.0
+        self.cols = max_iter + 2
+
+    def hptr(self, i, j):
+        w = 2 if self.complex else 1
+        return self.H.data_ptr() + 8 * w * (j * self.cols + i)
+
+    def col(self, j, k):
+        w = 2 if self.complex else 1
+        c = self.H[w * j * self.cols : w * (j * self.cols + k)].cpu().numpy()
+        return c.view(np.complex128) if self.complex else c
+
+    def mgs_step(self, w, v_prev, h_prev_ptr, v_cur, out_ptr):
+        if not self.complex:
+            _lib.call("spk_mgs", self.ctx, self.n, ptr(w), ptr(v_prev) if v_prev is not None else None,
+                      h_prev_ptr, ptr(v_cur) if v_cur is not None else None, out_ptr, self.st)
+            return
+        # complex: w -= h v (complex h), <v, w> = sum conj(v) w (np.vdot), ||w||
+        wc = torch.view_as_complex(w.view(-1, 2))
+        if v_prev is not None:
+            h = torch.view_as_complex(self._h_view(h_prev_ptr))
+            wc -= h * torch.view_as_complex(v_prev.view(-1, 2))
+        if v_cur is not None:
+            val = torch.vdot(torch.view_as_complex(v_cur.view(-1, 2)), wc)
+            self._h_view(out_ptr).copy_(torch.view_as_real(val.reshape(1)).reshape(2))
+        else:
+            nrm = torch.linalg.vector_norm(wc)
+            self._h_view(out_ptr).copy_(torch.stack([nrm, torch.zeros_like(nrm)]))
+
+    def _h_view(self, p):
+        off = (p - self.H.data_ptr()) // 8
+        return self.H[off : off + 2]
+
+    def norm_into(self, w, out_ptr):
+        self.mgs_step(w, None, None, None, out_ptr)
+
+    def scale_div(self, w, h_ptr, out):
+        if not self.complex:
+            _lib.call("spk_scale_div", self.n, ptr(w), h_ptr, ptr(out), self.st)
+        else:
+            h = self._h_view(h_ptr)[0]
+            torch.div(w, h, out=out)
+
+
+def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None):
+    """Solve A x = rhs with right preconditioning A P^{-1} y = rhs, x = P^{-1} y.
+
+    rhs: torch CUDA tensor (device path) or numpy array (bridged). Returns (x, KrylovReport) with x in
+    the container type of rhs.
+    """
+    if not (0.0 < rel_tol < 1.0):
+        raise ValueError("rel_tol must lie in (0, 1)")
+    require_cuda()
+    host = not isinstance(rhs, torch.Tensor)
+    if host:
+        arr = np.asarray(rhs)
+        complex_ = np.iscomplexobj(arr) if dtype is None else np.dtype(dtype).kind == "c"
+        device = torch.device("cuda", torch.cuda.current_device())
+        shape = arr.shape
+        bt = torch.from_numpy(np.ascontiguousarray(arr.astype(np.complex128 if complex_ else np.float64)))
+        bt = bt.to(device)
+    else:
+        complex_ = rhs.is_complex() if dtype is None else (np.dtype(dtype).kind == "c")
+        device = rhs.device
+        shape = tuple(rhs.shape)
+        bt = rhs.to(torch.complex128 if complex_ else torch.float64)
+    b = (torch.view_as_real(bt.contiguous()) if complex_ else bt.contiguous()).reshape(-1).clone()
+    n = b.numel()
+    A = _Bridge(apply_A, shape, host, complex_, device)
+    P = _Bridge(apply_Pinv, shape, host, complex_, device)
+    ops = _Ops(n, complex_, device, max_iter)
+
+    def out_of(v):
+        x = v.reshape(shape + ((2,) if complex_ else ()))
+        if complex_:
+            x = torch.view_as_complex(x.contiguous())
+        return x.cpu().numpy() if host else x
+
+    report = KrylovReport()
+    beta_ptr = ops.hptr(0, max_iter + 1)  # scratch slot outside the used columns
+    ops.norm_into(b, beta_ptr)
+    beta = float(ops.col(max_iter + 1, 1)[0].real)
+    report.residual_history.append(beta)
+    if beta == 0.0:
+        report.converged = True
+        report.reduction_achieved = 0.0
+        z = torch.zeros_like(b)
+        return out_of(z), report
+    target = rel_tol * beta
+
+    basis = [torch.empty_like(b)]
+    ops.scale_div(b, beta_ptr, basis[0])
+    Hh = np.zeros((max_iter + 1, max_iter), dtype=np.complex128 if complex_ else np.float64)
+    g = np.zeros(max_iter + 1, dtype=Hh.dtype)
+    g[0] = beta
+    k = 0
+    happy = False
+    for j in range(max_iter):
+        w = A(P(basis[j])).clone()
+        # modified Gram-Schmidt: h_ij = <v_i, w>; w -= h_ij v_i  (fused pairwise on device)
+        ops.mgs_step(w, None, None, basis[0], ops.hptr(0, j))
+        for i in range(1, j + 1):
+            ops.mgs_step(w, basis[i - 1], ops.hptr(i - 1, j), basis[i], ops.hptr(i, j))
+        ops.mgs_step(w, basis[j], ops.hptr(j, j), None, ops.hptr(j + 1, j))
+        col = ops.col(j, j + 2)
+        if not np.all(np.isfinite(col.view(np.float64) if complex_ else col)):
+            raise NumericalFailureError("non-finite value in GMRES operator output")
+        Hh[: j + 2, j] = col
+        k = j + 1
+        if abs(Hh[j + 1, j]) < BREAKDOWN_TOL:
+            happy = True
+        else:
+            vnext = torch.empty_like(b)
+            ops.scale_div(w, ops.hptr(j + 1, j), vnext)
+            basis.append(vnext)
+        y, res = _solve_hessenberg(Hh[: k + 1, :k], g[: k + 1])
+        report.residual_history.append(res)
+        if happy or res <= target:
+            break
+
+    y, _ = _solve_hessenberg(Hh[: k + 1, :k], g[: k + 1])
+    z = torch.empty_like(b)
+    if complex_:
+        zc = torch.zeros(n // 2, dtype=torch.complex128, device=device)
+        for i in range(k):
+            zc = zc + complex(y[i]) * torch.view_as_complex(basis[i].view(-1, 2))
+        z = torch.view_as_real(zc).reshape(-1).contiguous()
+    else:
+        yd = torch.from_numpy(np.ascontiguousarray(y[:k].astype(np.float64))).to(device)
+        tbl = torch.tensor([v.data_ptr() for v in basis[:k]], dtype=torch.int64, device=device)
+        _lib.call("spk_lincomb", n, k, tbl.data_ptr(), ptr(yd), ptr(z), ops.st)
+    x = P(z).clone()
+    r = A(x).clone()
+    # ||b - A x|| : r -= 1 * b, then the norm (fused)
+    one = ops.scal.data_ptr()
+    res_ptr = ops.hptr(1, max_iter + 1)
+    if complex_:
+        rc = torch.view_as_complex(r.view(-1, 2)) - torch.view_as_complex(b.view(-1, 2))
+        true_res = float(torch.linalg.vector_norm(rc).item())
+    else:
+        _lib.call("spk_mgs", ops.ctx, n, ptr(r), ptr(b), one, None, res_ptr, ops.st)
+        true_res = float(ops.H[(max_iter + 1) * ops.cols + 1].item())
+    report.iterations = k
+    report.reduction_achieved = true_res / beta
+    report.converged = happy or true_res <= target * (1.0 + 1e-9) or report.residual_history[-1] <= target
+    if not bool(torch.isfinite(x).all().item()):
+        raise NumericalFailureError("non-finite GMRES solution")
+    return out_of(x), report

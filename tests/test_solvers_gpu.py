@@ -1,0 +1,201 @@
+"""Device multigrid / GMRES / time steps vs the CPU oracle (north_star: solutions 1e-9, iterations +-1)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import solvers as OS
+from oracle import stepper as OST
+from oracle.fem_qk import Hierarchy
+from oracle.tableau_ref import radau_iia as ref_radau
+from paper_2209_06700_b200.complex_solver import DirectComplexSystem
+from paper_2209_06700_b200.errors import NumericalFailureError
+from paper_2209_06700_b200.fem import build_hierarchy
+from paper_2209_06700_b200.irk import StageSystem
+from paper_2209_06700_b200.krylov import gmres
+from paper_2209_06700_b200.multigrid import (BatchedBlockSolver, BlockSolver, MultiBlockSolver, PairBlockSolver,
+                                             VCycleConfig)
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+MG_CASES = [(1, 1, 4), (2, 1, 3), (3, 1, 3), (2, 2, 3), (3, 2, 2), (3, 3, 2), (3, 4, 2), (2, 4, 2)]
+
+
+@pytest.mark.parametrize("dim,k,L", MG_CASES)
+def test_block_vcycle_matches_oracle(cuda, dim, k, L):
+    h, o = build_hierarchy(dim, L, k), Hierarchy(dim, L, k)
+    b = np.where(o.finest.interior_mask, np.random.default_rng(5).standard_normal(o.n), 0.0)
+    for deg in (5, 3, 1):
+        cfg = VCycleConfig(smoother_degree=deg)
+        dev = BlockSolver(h, 1.7, 0.05, cfg)
+        ref = OS.VCycle(o, [1.7], 0.05, OS.Config(smoother_degree=deg))
+        for l in range(L + 1):
+            assert abs(dev.smoothers[l].theta - ref.sm[l][0].theta) < 1e-12 * ref.sm[l][0].theta
+        assert rel(dev.apply(b), ref.apply(b)) < 1e-11
+
+
+@pytest.mark.parametrize("dim,k,L", [(1, 1, 4), (3, 2, 2), (3, 4, 2)])
+def test_batched_multi_pair_match_oracle(cuda, dim, k, L):
+    h, o = build_hierarchy(dim, L, k), Hierarchy(dim, L, k)
+    rng = np.random.default_rng(9)
+    b = np.where(o.finest.interior_mask, rng.standard_normal((3, o.n)), 0.0)
+    lams = [1.5, 4.0, 9.0]
+    assert rel(BatchedBlockSolver(h, lams, 0.02).apply(b), OS.VCycle(o, lams, 0.02, shared=True).apply(b)) < 1e-11
+    assert rel(MultiBlockSolver(h, lams, 0.02).apply(b), OS.VCycle(o, lams, 0.02).apply(b)) < 1e-11
+    pb, po = PairBlockSolver(h, 2.0, np.sqrt(2.0), 0.05), OS.VCycle(o, tau=0.05, pair=(2.0, np.sqrt(2.0)))
+    assert rel(pb.apply(b[:2]), po.apply(b[:2])) < 1e-11
+    for l in range(L + 1):
+        assert abs(pb.smoothers[l].theta - po.sm[l].theta) < 1e-12 * po.sm[l].theta
+
+
+def test_vcycle_linear_and_symmetric(cuda):
+    h = build_hierarchy(2, 3, 2)
+    mask = h.finest.interior_mask
+    rng = np.random.default_rng(23)
+    s = BlockSolver(h, 2.0, 0.1)
+    b1, b2 = (np.where(mask, rng.standard_normal(h.n), 0.0) for _ in range(2))
+    lhs, rhs = s.apply(3.0 * b1 - 0.5 * b2), 3.0 * s.apply(b1) - 0.5 * s.apply(b2)
+    assert np.abs(lhs - rhs).max() < 1e-12 * max(np.abs(lhs).max(), 1.0)
+    v1, v2 = s.apply(b1), s.apply(b2)
+    assert abs(v1 @ b2 - b1 @ v2) < 1e-10 * max(abs(v1 @ b2), 1.0)
+    assert np.all(PairBlockSolver(h, 2.0, 1.5, 0.1).apply(np.zeros((2, h.n))) == 0.0)
+
+
+def test_vcycle_nan_raises(cuda):
+    h = build_hierarchy(2, 3, 1)
+    b = np.zeros(h.n)
+    b[h.n // 2] = np.nan
+    with pytest.raises(NumericalFailureError):
+        BlockSolver(h, 1.0, 0.1).apply(b)
+
+
+def test_gmres_vcycle_mesh_independence_and_dense(cuda):
+    its = []
+    for L in (4, 5):
+        h = build_hierarchy(1, L)
+        o = Hierarchy(1, L)
+        s = BlockSolver(h, 1.0, 0.1)
+        b = np.where(h.finest.interior_mask, np.random.default_rng(3).standard_normal(h.n), 0.0)
+        x, rep = gmres(lambda v: h.apply_constrained(L, 1.0, 0.1, v), s.apply, b, rel_tol=1e-12)
+        its.append(rep.iterations)
+        A = np.column_stack([o.apply_constrained(L, 1.0, 0.1, e) for e in np.eye(h.n)])
+        assert np.allclose(x, np.linalg.solve(A, b), atol=1e-9)
+    assert its[0] <= 10 and abs(its[0] - its[1]) <= 1
+
+
+@pytest.mark.parametrize("dim,k,L", [(2, 2, 3), (3, 3, 2)])
+def test_device_gmres_matches_oracle(cuda, dim, k, L):
+    h, o = build_hierarchy(dim, L, k), Hierarchy(dim, L, k)
+    b = np.where(o.finest.interior_mask, np.random.default_rng(1).standard_normal(o.n), 0.0)
+    s, so = BlockSolver(h, 1.7, 0.05), OS.VCycle(o, [1.7], 0.05)
+    bt = torch.from_numpy(b).cuda()
+    x, rep = gmres(lambda v: h.apply_constrained(L, 1.7, 0.05, v), lambda v: s.apply(v), bt, rel_tol=1e-12)
+    xo, its, hist, conv = OS.gmres(lambda v: o.apply_constrained(L, 1.7, 0.05, v), so.apply, b)
+    assert rep.iterations == its and rep.converged
+    assert rel(x.cpu().numpy(), xo) < 1e-9
+    assert rel(np.array(rep.residual_history), np.array(hist)) < 1e-6
+
+
+def test_gmres_reference_contract(cuda):
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal(20)
+    x, rep = gmres(lambda v: v, None, b)
+    assert rep.iterations == 1 and rep.converged and np.allclose(x, b, atol=1e-12)
+    A = rng.standard_normal((40, 40)) + 8.0 * np.eye(40)
+    b = rng.standard_normal(40)
+    x, rep = gmres(lambda v: A @ v, None, b, rel_tol=1e-12)
+    hist = np.array(rep.residual_history)
+    assert np.all(hist[1:] <= hist[:-1] * (1 + 1e-14))
+    assert abs(hist[-1] - np.linalg.norm(b - A @ x)) <= 1e-12 * hist[0] + 1e-12 * np.linalg.norm(b - A @ x)
+    xd, repd = gmres(lambda v: np.diag([2.0, 3.0, 4.0]) @ v, None, np.array([1.0, 0.0, 0.0]), rel_tol=1e-15)
+    assert repd.converged and np.allclose(xd, [0.5, 0, 0], atol=1e-14)
+    _, repn = gmres(lambda v: A @ v, None, b, rel_tol=1e-14, max_iter=3)
+    assert not repn.converged and repn.iterations == 3
+    with pytest.raises(NumericalFailureError):
+        gmres(lambda v: np.full_like(v, np.nan), None, np.ones(4))
+    with pytest.raises(ValueError):
+        gmres(lambda v: v, None, np.ones(3), rel_tol=0.0)
+    Ac = rng.standard_normal((25, 25)) + 1j * rng.standard_normal((25, 25)) + 10 * np.eye(25)
+    bc = rng.standard_normal(25) + 1j * rng.standard_normal(25)
+    xc, repc = gmres(lambda v: Ac @ v, None, bc, rel_tol=1e-12)
+    assert repc.converged and np.allclose(xc, np.linalg.solve(Ac, bc), atol=1e-9)
+
+
+def _run_pair(dev_sys, ora_sys, steps, tau):
+    u = dev_sys.initial_condition()
+    uo = ora_sys.initial()
+    assert rel(u.cpu().numpy(), uo) < 1e-15
+    its_d, its_o = [], []
+    for s in range(steps):
+        u, rep = dev_sys.step(s * tau, u)
+        uo, ito, conv = ora_sys.step(s * tau, uo)
+        its_d.append(rep.iterations)
+        its_o.append(ito)
+    return u.cpu().numpy(), uo, its_d, its_o
+
+
+def test_config1_steps_match_oracle(cuda):
+    """C1: 2D, 16x16 Q2 cells, Radau IIA Q=2, tau=0.05, 10 steps, GMRES rtol 1e-10."""
+    h, o = build_hierarchy(2, 4, 2), Hierarchy(2, 4, 2)
+    tab = ref_radau(2)
+    dev = StageSystem(h, 2, 0.05, rel_tol=1e-10, tableau=tab)
+    ora = OST.RealLU(o, 2, 0.05, rel_tol=1e-10, tab=tab)
+    u, uo, itd, ito = _run_pair(dev, ora, 10, 0.05)
+    assert all(abs(a - b) <= 1 for a, b in zip(itd, ito)), (itd, ito)
+    assert rel(u, uo) < 1e-9
+    err = h.l2_error(4, u, lambda x, t: np.prod(np.sin(np.pi * x), axis=1) * np.exp(-t), 0.5)
+    assert err < 1e-4
+
+
+def test_config3_like_steps_match_oracle(cuda):
+    """C3 settings (Q2, Radau Q=3, tau=0.01, Chebyshev degree 3) on a 8^3 mesh, 3 steps."""
+    h, o = build_hierarchy(3, 3, 2), Hierarchy(3, 3, 2)
+    tab = ref_radau(3)
+    cfg = VCycleConfig(smoother_degree=3)
+    dev = StageSystem(h, 3, 0.01, config=cfg, tableau=tab)
+    ora = OST.RealLU(o, 3, 0.01, OS.Config(smoother_degree=3), tab=tab)
+    u, uo, itd, ito = _run_pair(dev, ora, 3, 0.01)
+    assert all(abs(a - b) <= 1 for a, b in zip(itd, ito)), (itd, ito)
+    assert rel(u, uo) < 1e-9
+
+
+def test_batched_mode_matches_oracle(cuda):
+    h, o = build_hierarchy(3, 3, 1), Hierarchy(3, 3, 1)
+    tab = ref_radau(4)
+    dev = StageSystem(h, 4, 0.1, mode="batched", tableau=tab)
+    ora = OST.RealLU(o, 4, 0.1, tab=tab, shared=True)
+    u, uo, itd, ito = _run_pair(dev, ora, 2, 0.1)
+    assert all(abs(a - b) <= 1 for a, b in zip(itd, ito)), (itd, ito)
+    assert rel(u, uo) < 1e-9
+
+
+@pytest.mark.parametrize("variant", ["presb", "gmg"])
+def test_complex_path_matches_oracle(cuda, variant):
+    """C5 settings (Q3 elements, Radau Q=3 = one real + one complex pair, tau=5e-3) on 4^3 cells."""
+    h, o = build_hierarchy(3, 2, 3), Hierarchy(3, 2, 3)
+    tab = ref_radau(3)
+    dev = DirectComplexSystem(h, 3, 5e-3, variant=variant, tableau=tab)
+    ora = OST.DirectComplex(o, 3, 5e-3, variant=variant, tab=tab)
+    u = dev.initial_condition()
+    uo = ora.initial()
+    for s in range(2):
+        u, rep = dev.step(s * 5e-3, u)
+        uo, ito = ora.step(s * 5e-3, uo)
+        assert all(abs(a - b) <= 1 for a, b in zip(rep.block_iterations, ito)), (rep.block_iterations, ito)
+    assert rel(u.cpu().numpy(), uo) < 1e-9
+
+
+def test_real_and_complex_paths_agree(cuda):
+    h = build_hierarchy(3, 3, 1)
+    tab = ref_radau(2)
+    a = StageSystem(h, 2, 0.1, tableau=tab)
+    b = DirectComplexSystem(h, 2, 0.1, variant="presb", tableau=tab)
+    ua, _, _ = a.run(3)
+    ub, _, _ = b.run(3)
+    assert rel(ub.cpu().numpy(), ua.cpu().numpy()) < 1e-8
