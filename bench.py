@@ -205,12 +205,23 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(s)
-    for _ in range(args.steps):
-        u.copy_(u_host, non_blocking=True)
-        apply_dev()
-        v_host.copy_(v, non_blocking=True)
-    e3.record(s)
+    if world == 1:
+        # public host-buffer entry point: chunked H2D / K1 / D2H overlap (pipeline.py)
+        from paper_2209_06700_b200.pipeline import HostStageOperator
+        hop = HostStageOperator(hier, L, DM, DK)
+        hop.apply(u_host, v_host)
+        torch.cuda.synchronize()
+        e2.record(s)
+        for _ in range(args.steps):
+            hop.apply(u_host, v_host)
+        e3.record(s)
+    else:
+        e2.record(s)
+        for _ in range(args.steps):
+            u.copy_(u_host, non_blocking=True)
+            apply_dev()
+            v_host.copy_(v, non_blocking=True)
+        e3.record(s)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3) / args.steps
     if world > 1:

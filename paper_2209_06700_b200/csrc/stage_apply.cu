@@ -46,7 +46,7 @@ template <int K, int Q> struct Geo {
   static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ;
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
-  static constexpr int ZS = (Q >= 2) ? 2 : 1;
+  static constexpr int ZS = 1;
   static constexpr int ZSEG = (TZE + ZS - 1) / ZS;
   static constexpr int ZITEMS = Q * NYin * ZSEG;
   static constexpr int ZIT = (ZITEMS + NT - 1) / NT;
@@ -105,6 +105,8 @@ template <int K> struct Coef {
   __device__ __forceinline__ double m(int r, int s) const { return mv[Sym<K>::cls(r, s)]; }
   __device__ __forceinline__ double s(int r, int s2) const { return sv[Sym<K>::cls(r, s2)]; }
 };
+
+template <int V> struct IC { static constexpr int value = V; };
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -343,6 +345,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
 
   // ---- fixed per-thread work descriptors ----
   const long long plane_stride = (long long)g.ny * g.nz;
+  // U-plane load items: slots outside the domain are zeroed once (in both buffers) and never
+  // loaded; in-domain slots get one 8-byte cp.async per plane (zero-fill only for constrained
+  // boundary nodes).
   const double* lsrc[G::LIT];
   unsigned ldst[G::LIT];
   bool lbnd[G::LIT];
@@ -350,33 +355,44 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
   for (int i = 0; i < G::LIT; ++i) {
     const int idx = tid + i * NT;
     lsrc[i] = nullptr;
-    ldst[i] = 0xffffffffu;
+    ldst[i] = 0u;
     lbnd[i] = false;
     if (idx < G::LITEMS) {
       const int q = idx / (NYin * NZin);
       const int rem = idx - q * (NYin * NZin);
       const int yy = rem / NZin, zz = rem - yy * NZin;
       const int gy = y_lo - K + yy, gz = z_lo - K + zz;
-      ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + (q * NYin + yy) * NZp + zz));
+      const int slot = (q * NYin + yy) * NZp + zz;
       if (gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz) {
+        ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
         lsrc[i] = u + (long long)q * a.su + (long long)gy * g.nz + gz;
         lbnd[i] = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
+      } else {
+        Us[slot] = 0.0;
+        Us[G::U_SZ + slot] = 0.0;
       }
     }
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
   auto load_plane = [&](int x, int buf) {
-    const bool xb = !xdeg && (x == 0 || x == g.nx - 1);
     const long long xoff = (long long)x * plane_stride;
+    if (!a.constrained) {
 #pragma unroll
-    for (int i = 0; i < G::LIT; ++i) {
-      if (ldst[i] == 0xffffffffu) continue;
-      bool in = lsrc[i] != nullptr;
-      if (a.constrained) in = in && !(xb || lbnd[i]);
-      const double* src = in ? lsrc[i] + xoff : u;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
-                   "l"(src), "r"(in ? 8 : 0) : "memory");
+      for (int i = 0; i < G::LIT; ++i) {
+        if (lsrc[i] == nullptr) continue;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ldst[i] + buf * UBUF),
+                     "l"(lsrc[i] + xoff) : "memory");
+      }
+    } else {
+      const bool xb = !xdeg && (x == 0 || x == g.nx - 1);
+#pragma unroll
+      for (int i = 0; i < G::LIT; ++i) {
+        if (lsrc[i] == nullptr) continue;
+        const int nb = (xb || lbnd[i]) ? 0 : 8;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
+                     "l"(lsrc[i] + xoff), "r"(nb) : "memory");
+      }
     }
     cp_async_commit();
   };
@@ -402,7 +418,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
   int yoff[G::YIT], yeb[G::YIT];
 #pragma unroll
   for (int i = 0; i < G::YIT; ++i) {
-    const int it = tid + i * NT;
+    // Y items are placed on the threads with the fewest Z items (balance inside the interval)
+    constexpr int YOFF = (G::YITEMS % NT == 0) ? 0 : NT - (G::YITEMS % NT);
+    const int it = (tid + NT - YOFF) % NT + i * NT;
     yeb[i] = TYE;
     yoff[i] = 0;
     if (it < G::YITEMS) {
@@ -445,7 +463,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
 #pragma unroll
           for (int r = 0; r < K; ++r) {
             const int zl = K * e + r;
-            if (r == 0 || zl < nzo) { arow[zl] = oa[r]; brow[zl] = ob[r]; }
+            arow[zl] = oa[r];  // zl < TZ always; columns >= nzo are never read
+            brow[zl] = ob[r];
           }
 #pragma unroll
           for (int s = 0; s <= K; ++s) L[s] = R[s];
@@ -502,11 +521,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
           elem3<K>(cf, La, Ra, Lb, Rb, wl, wr, om, oc);
 #pragma unroll
           for (int r = 0; r < K; ++r) {
-            const int yl = K * e + r;
-            if (r == 0 || yl < nyo) {
-              mcol[yl * TZp] = om[r];
-              ccol[yl * TZp] = oc[r];
-            }
+            const int yl = K * e + r;  // yl < TY always; rows >= nyo are never read
+            mcol[yl * TZp] = om[r];
+            ccol[yl * TZp] = oc[r];
           }
 #pragma unroll
           for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
@@ -534,15 +551,18 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
   const bool dm_ident = a.dm_identity != 0;
 
   // ---------------- X-phase: stage mix + element-push accumulation ----------------
-  auto xphase = [&](int x, int mc) {
+  // the plane's local index r within element ecur is uniform: dispatch to a copy with the x-table
+  // column as compile-time register operands
+  auto xphase_r = [&](auto RC, int x, int mc) {
+    constexpr int RR = decltype(RC)::value;
     const double* MAs = MCs + mc * 2 * G::MC_SZ;
     const double* Cs = MAs + G::MC_SZ;
-    const int r_loc = xdeg ? 0 : x - K * ecur;   // local plane index within element ecur (0..K)
+    constexpr int r_loc = RR;
     double cmx[K + 1], ckx[K + 1];
 #pragma unroll
     for (int s = 0; s <= K; ++s) {
-      cmx[s] = c_hat[K - 1][0][s][r_loc];
-      ckx[s] = c_hat[K - 1][1][s][r_loc];
+      cmx[s] = cf.m(s, RR);
+      ckx[s] = cf.s(s, RR);
     }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -622,6 +642,16 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
       }
     }
     if (!xdeg && r_loc == K) ++ecur;
+  };
+  auto xphase = [&](int x, int mc) {
+    const int r_loc = xdeg ? 0 : x - K * ecur;   // 0..K
+    switch (r_loc) {
+      case 0: xphase_r(IC<0>{}, x, mc); break;
+      case 1: xphase_r(IC<1>{}, x, mc); break;
+      case 2: if constexpr (K >= 2) xphase_r(IC<2>{}, x, mc); break;
+      case 3: if constexpr (K >= 3) xphase_r(IC<3>{}, x, mc); break;
+      case 4: if constexpr (K >= 4) xphase_r(IC<4>{}, x, mc); break;
+    }
   };
 
   if constexpr (G::PIPE3) {
