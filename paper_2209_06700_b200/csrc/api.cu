@@ -184,23 +184,32 @@ int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a0, 
 int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, int lam_uniform,
                          double tau, int constrained, int epi, SpkApplyArgs a, cudaStream_t s,
                          const double* c1s, const double* c2s) {
-  // launch in groups of SPK_BMAX blocks so per-block coefficients fit the parameter block
-  for (int b0 = 0; b0 < nblk; b0 += (lam_uniform && !c1s && !c2s) ? nblk : SPK_BMAX) {
-    const int nb = (lam_uniform && !c1s && !c2s) ? nblk : std::min(SPK_BMAX, nblk - b0);
+  // launch in groups of at most SPK_BMAX blocks so per-block coefficients fit the parameter block;
+  // inside a launch every CTA sweeps `per_cta` blocks together (1..4) to share the halo loads,
+  // index math and barriers of the plane pipeline
+  for (int b0 = 0; b0 < nblk;) {
+    int nb = std::min(SPK_BMAX, nblk - b0);
+    int per_cta = 1;
+    for (int q = 4; q >= 2; --q)
+      if (nb >= q) { per_cta = q; break; }
+    nb = (nb / per_cta) * per_cta;
     a.blk_base = b0;
     a.nblk = nb;
     a.lam_uniform = lam_uniform;
     a.tau = tau;
     a.constrained = constrained;
-    for (int i = 0; i < (lam_uniform ? 1 : nb); ++i) a.lam[i] = lams[b0 + i];
+    if (lam_uniform) a.lam[0] = lams[0];
+    else
+      for (int i = 0; i < nb; ++i) a.lam[i] = lams[b0 + i];
     for (int i = 0; i < nb && i < SPK_BMAX; ++i) {
       a.c1[i] = c1s ? c1s[b0 + i] : 0.0;
       a.c2[i] = c2s ? c2s[b0 + i] : 0.0;
     }
-    set_chunking(c, a, c->K, nb);
+    set_chunking(c, a, c->K, nb / per_cta);
     // blocks are addressed as blk*su from the base pointer, so pass the unshifted base
-    int rc = launch_apply(c, 1, true, epi, a, s);
+    int rc = launch_apply(c, per_cta, true, epi, a, s);
     if (rc) return rc;
+    b0 += nb;
   }
   return SPK_OK;
 }

@@ -1,0 +1,754 @@
+// K1: batched / stage-coupled matrix-free Q_k operator on the uniform grid, sm_100a, fp64.
+//
+//   coupled mode : v_i = sum_j ( DM_ij M + DK_ij K ) u_j        i,j < Q      (I(x)M + tau A(x)K, ...)
+//   block mode   : v_b = lam_b M u_b + tau K u_b                 b < nblk     (lam M + tau K per block)
+//
+// M = Mx(x)My(x)Mz and K = Kx My Mz + Mx Ky Mz + Mx My Kz are the Kronecker forms the reference
+// applies with dense 1D contractions (fem.py:120-151, _contract fem.py:37-41). Here the assembled
+// 1D matrices are never formed: each axis is applied element-by-element from the (k+1)x(k+1)
+// reference-element tables (compile-time constants, spk_tables.cuh), which is the flop-minimal
+// banded form (SURVEY.md §7 hard part 1). The mesh size is folded into the stage mix:
+// M = h^d M_hat, K = h^(d-2) K_hat, so the host passes DM' = h^d DM and DK' = h^(d-2) DK.
+//
+// Schedule ("2.5D sliding window", one CTA = one (y,z) tile x one x-chunk, all Q stages):
+//   per x-plane:  cp.async plane x+1 into the other smem buffer (double buffering)
+//                 Z-phase   a = Mz u, b = Kz u                 (smem -> smem, 2 elements / item)
+//                 Y-phase   ma = My a, c = Ky a + My b          (smem -> smem, 2 elements / item)
+//                 X-phase   stage mix p_i = sum_j DM_ij ma_j + DK_ij c_j, q_i = sum_j DK_ij ma_j
+//                           and element-push accumulation v += Mx[.,r] p + Kx[.,r] q in registers
+//   an element's K output planes are finished when its last plane arrives -> fused epilogue.
+// Every thread's work items are fixed for the whole kernel (no per-plane index arithmetic).
+// HBM traffic per apply: read u once (+ L2-resident halo), write v once = 16 B per stage-DoF.
+#pragma once
+#include "spk_internal.cuh"
+#include "spk_tables.cuh"
+
+namespace {
+
+template <int K> struct Tile;
+template <> struct Tile<1> { static constexpr int TYE = 16, TZE = 32; };
+template <> struct Tile<2> { static constexpr int TYE = 8, TZE = 16; };
+template <> struct Tile<3> { static constexpr int TYE = 5, TZE = 11; };
+template <> struct Tile<4> { static constexpr int TYE = 4, TZE = 8; };
+
+template <int K, int Q> struct Geo {
+  static constexpr int TYE = Tile<K>::TYE, TZE = Tile<K>::TZE;
+  static constexpr int TY = K * TYE, TZ = K * TZE;
+  // 1 barrier per plane: Z, Y, X run on three plane buffers (see the pipeline below)
+  static constexpr bool PIPE3 = true;
+  static constexpr int NT = (Q >= 2) ? 512 : 256;
+  static constexpr int NBUF = PIPE3 ? 2 : 1;
+  static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
+  static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
+  static constexpr int TZp = TZ | 1;
+  static constexpr int U_SZ = Q * NYin * NZp;          // one plane buffer
+  static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
+  static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ;
+  static constexpr int PPT = (TY * TZ + NT - 1) / NT;
+  // Z items: (q, yy, element segment), ZS elements per segment
+  static constexpr int ZS = 1;
+  static constexpr int ZSEG = (TZE + ZS - 1) / ZS;
+  static constexpr int ZITEMS = Q * NYin * ZSEG;
+  static constexpr int ZIT = (ZITEMS + NT - 1) / NT;
+  // Y items: (q, z, element segment)
+  static constexpr int YS = 1;
+  static constexpr int YSEG = (TYE + YS - 1) / YS;
+  static constexpr int YITEMS = Q * TZ * YSEG;
+  static constexpr int YIT = (YITEMS + NT - 1) / NT;
+  // U load items
+  static constexpr int LITEMS = Q * NYin * NZin;
+  static constexpr int LIT = (LITEMS + NT - 1) / NT;
+  static constexpr int MINB = (!PIPE3 && SMEM_DOUBLES * 8 <= 113 * 1024) ? 2 : 1;
+};
+
+// Distinct entries of a symmetric, centro-symmetric (K+1)x(K+1) element table:
+// (r,s) ~ (s,r) ~ (K-r,K-s) ~ (K-s,K-r). cls() maps an entry to its class, NC classes in total.
+template <int K> struct Sym {
+  __host__ __device__ static constexpr int canon(int r, int s) {
+    int best = r * 16 + s;
+    const int c2 = s * 16 + r, c3 = (K - r) * 16 + (K - s), c4 = (K - s) * 16 + (K - r);
+    if (c2 < best) best = c2;
+    if (c3 < best) best = c3;
+    if (c4 < best) best = c4;
+    return best;
+  }
+  __host__ __device__ static constexpr int cls(int r, int s) {
+    const int me = canon(r, s);
+    int n = 0;
+    for (int a = 0; a <= K; ++a)
+      for (int b = 0; b <= K; ++b)
+        if (canon(a, b) == a * 16 + b && a * 16 + b < me) ++n;
+    return n;
+  }
+  __host__ __device__ static constexpr int count() {
+    int n = 0;
+    for (int a = 0; a <= K; ++a)
+      for (int b = 0; b <= K; ++b)
+        if (canon(a, b) == a * 16 + b) ++n;
+    return n;
+  }
+};
+
+// reference-element mass (M) and stiffness (S) tables held in registers
+template <int K> struct Coef {
+  static constexpr int NC = Sym<K>::count();
+  double mv[NC], sv[NC];
+  __device__ __forceinline__ void load() {
+#pragma unroll
+    for (int r = 0; r <= K; ++r)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) {
+        mv[Sym<K>::cls(r, s)] = c_hat[K - 1][0][r][s];
+        sv[Sym<K>::cls(r, s)] = c_hat[K - 1][1][r][s];
+      }
+  }
+  __device__ __forceinline__ double m(int r, int s) const { return mv[Sym<K>::cls(r, s)]; }
+  __device__ __forceinline__ double s(int r, int s2) const { return sv[Sym<K>::cls(r, s2)]; }
+};
+
+template <int V> struct IC { static constexpr int value = V; };
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// assembled 1D reference diagonal at node i of an axis with E elements (E == 0: degenerate axis)
+template <int K>
+__device__ __forceinline__ void diag1(int i, int E, double& dm, double& dk) {
+  using H = Hat<K>;
+  if (E == 0) { dm = 1.0; dk = 0.0; return; }
+  const int e = i / K, r = i - e * K;
+  if (r != 0) {
+    double m = 0.0, s = 0.0;
+#pragma unroll
+    for (int rr = 1; rr < K; ++rr)
+      if (rr == r) { m = H::M(rr, rr); s = H::S(rr, rr); }
+    dm = m; dk = s;
+    return;
+  }
+  dm = 0.0; dk = 0.0;
+  if (e > 0) { dm += H::M(K, K); dk += H::S(K, K); }
+  if (e < E) { dm += H::M(0, 0); dk += H::S(0, 0); }
+}
+
+// reference-element diagonal pieces at a node (association order of np.multiply.outer chains,
+// reference fem.py:172-187); the caller scales by DM' / DK'
+template <int K>
+__device__ __forceinline__ void node_diag(const SpkDims& g, int x, int y, int z, double& dm, double& dk) {
+  double mx, kx, my, ky, mz, kz;
+  diag1<K>(x, g.Ex, mx, kx);
+  diag1<K>(y, g.Ey, my, ky);
+  diag1<K>(z, g.Ez, mz, kz);
+  dm = (mx * my) * mz;
+  dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+}
+
+__device__ __forceinline__ bool on_boundary(const SpkDims& g, int x, int y, int z) {
+  return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+         (g.Ez > 0 && (z == 0 || z == g.nz - 1));
+}
+
+// z-sweep of one element: vertex r=0 gathers the left element (row K) and the right element
+// (row 0); interior r>=1 use the right element only. Outputs a = M_hat u, b = K_hat u.
+template <int K>
+__device__ __forceinline__ void elem2(const Coef<K>& cf, const double (&L)[K + 1], const double (&R)[K + 1],
+                                      double wl, double wr, double (&o1)[K], double (&o2)[K]) {
+  double l1 = 0.0, l2 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+  for (int s = 0; s <= K; ++s) {
+    l1 = fma(cf.m(K, s), L[s], l1);
+    l2 = fma(cf.s(K, s), L[s], l2);
+    r1 = fma(cf.m(0, s), R[s], r1);
+    r2 = fma(cf.s(0, s), R[s], r2);
+  }
+  o1[0] = fma(wl, l1, wr * r1);
+  o2[0] = fma(wl, l2, wr * r2);
+#pragma unroll
+  for (int r = 1; r < K; ++r) {
+    double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      a1 = fma(cf.m(r, s), R[s], a1);
+      a2 = fma(cf.s(r, s), R[s], a2);
+    }
+    o1[r] = a1;
+    o2[r] = a2;
+  }
+}
+
+// y-sweep of one element on two inputs: ma = M_hat a ; c = K_hat a + M_hat b
+template <int K>
+__device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 1],
+                                      const double (&Ra)[K + 1], const double (&Lb)[K + 1],
+                                      const double (&Rb)[K + 1], double wl, double wr, double (&ma)[K],
+                                      double (&c)[K]) {
+  double lm = 0.0, lc = 0.0, rm = 0.0, rc = 0.0;
+#pragma unroll
+  for (int s = 0; s <= K; ++s) {
+    lm = fma(cf.m(K, s), La[s], lm);
+    lc = fma(cf.s(K, s), La[s], lc);
+    lc = fma(cf.m(K, s), Lb[s], lc);
+    rm = fma(cf.m(0, s), Ra[s], rm);
+    rc = fma(cf.s(0, s), Ra[s], rc);
+    rc = fma(cf.m(0, s), Rb[s], rc);
+  }
+  ma[0] = fma(wl, lm, wr * rm);
+  c[0] = fma(wl, lc, wr * rc);
+#pragma unroll
+  for (int r = 1; r < K; ++r) {
+    double am = 0.0, ac = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      am = fma(cf.m(r, s), Ra[s], am);
+      ac = fma(cf.s(r, s), Ra[s], ac);
+      ac = fma(cf.m(r, s), Rb[s], ac);
+    }
+    ma[r] = am;
+    c[r] = ac;
+  }
+}
+
+// Fused epilogue at one node for all Q stages / blocks of the CTA. Block mode: stage q of the CTA is
+// block b0 + q with its own shift lam[q] (and Chebyshev coefficients in its parameter slot).
+template <int K, int Q, bool BLOCK, int EPI>
+__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q], int x, int y,
+                                         int z, const double (&val)[Q], double& sumsq) {
+  const SpkDims& g = a.g;
+  const long long gi = ((long long)x * g.ny + y) * g.nz + z;
+  const bool bnd = a.constrained && on_boundary(g, x, y, z);
+  const long long ubase = BLOCK ? (long long)b0 * a.su : 0;
+  const long long ebase = BLOCK ? (long long)b0 * a.se : 0;
+  const long long vbase = BLOCK ? (long long)b0 * a.sv : 0;
+  const int slot0 = BLOCK ? b0 - a.blk_base : 0;
+  double Av[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) Av[q] = bnd ? __ldg(a.u + ubase + q * a.su + gi) : val[q];
+
+  if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) __stcs(a.v + vbase + q * a.sv + gi, Av[q]);
+  } else {
+    // Jacobi diagonal (analytic; reference operator_diagonal fem.py:172-187, 1.0 on boundary)
+    double dm, dk;
+    node_diag<K>(g, x, y, z, dm, dk);
+    double z0[Q];  // Dinv applied to the quantity of the epilogue
+    auto jacobi = [&](const double (&rr)[Q]) {
+      if constexpr (BLOCK) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) z0[q] = (bnd ? 1.0 : 1.0 / (lamq[q] * dm + a.tau * dk)) * rr[q];
+      } else {  // pair 2x2 block Jacobi (multigrid.py:268-276, 306-313)
+        const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
+        const double db = bnd ? 0.0 : a.jim * dm;
+        const double det = da * da + db * db;
+        const double A_ = da / det, B_ = db / det;
+        z0[0] = A_ * rr[0] + B_ * rr[1];
+        if constexpr (Q > 1) z0[1] = -B_ * rr[0] + A_ * rr[1];
+      }
+    };
+    if constexpr (EPI == EPI_DINV) {
+      jacobi(Av);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        a.v[vbase + q * a.sv + gi] = z0[q];
+        sumsq = fma(z0[q], z0[q], sumsq);
+      }
+    } else {
+      double rn[Q];
+      if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          rn[q] = __ldg(a.b + ebase + q * a.se + gi) - Av[q];
+          a.r[ebase + q * a.se + gi] = rn[q];
+        }
+      } else {  // EPI_CHEB:  x += d ; r -= A d ; d = c1 d + c2 Dinv r   (multigrid.py:82-87)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double dq = __ldg(a.u + ubase + q * a.su + gi);
+          rn[q] = a.r[ebase + q * a.se + gi] - Av[q];
+          a.r[ebase + q * a.se + gi] = rn[q];
+          a.x[ebase + q * a.se + gi] = a.x[ebase + q * a.se + gi] + dq;
+        }
+      }
+      if (a.d_out != nullptr) {
+        jacobi(rn);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int slot = BLOCK ? slot0 + q : 0;
+          double dn;
+          if constexpr (EPI == EPI_CHEB) {
+            const double dq = __ldg(a.u + ubase + q * a.su + gi);
+            dn = a.c1[slot] * dq + a.c2[slot] * z0[q];
+          } else {
+            dn = z0[q] / a.c2[slot];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
+          }
+          a.d_out[ebase + q * a.se + gi] = dn;
+        }
+      }
+    }
+  }
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+__global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
+    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
+  using G = Geo<K, Q>;
+  constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;
+  constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
+  constexpr int PPT = G::PPT;
+
+  extern __shared__ double smem[];
+  double* Us = smem;                    // [2][Q][NYin][NZp]
+  double* ABs = Us + 2 * G::U_SZ;       // [2][A|B][Q][NYin][TZp]
+  double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][MA|C][Q][TY][TZp]
+
+  const int tid = threadIdx.x;
+  const SpkDims g = a.g;
+  const bool ydeg = (g.Ey == 0), xdeg = (g.Ex == 0);
+  const int ez0 = blockIdx.x * TZE, ey0 = blockIdx.y * TYE;
+  const int chunk = blockIdx.z % a.nchunks;
+  const int b0 = BLOCK ? (a.blk_base + (int)(blockIdx.z / a.nchunks) * Q) : 0;  // first block of CTA
+
+  const int z_lo = K * ez0, z_hi = min(K * (ez0 + TZE), g.nz);
+  const int y_lo = ydeg ? 0 : K * ey0, y_hi = ydeg ? 1 : min(K * (ey0 + TYE), g.ny);
+  const int nzo = z_hi - z_lo, nyo = y_hi - y_lo;
+  const int nez = min(TZE, g.Ez + 1 - ez0);            // includes the virtual last-vertex element
+  const int ney = ydeg ? 1 : min(TYE, g.Ey + 1 - ey0);
+  const double* __restrict__ u = a.u + (BLOCK ? (long long)b0 * a.su : 0);
+
+  double lamq[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) lamq[q] = BLOCK ? (a.lam_uniform ? a.lam[0] : a.lam[b0 - a.blk_base + q]) : 0.0;
+
+  // reference-element tables in registers (distinct entries only)
+  Coef<K> cf;
+  cf.load();
+
+  // x-chunk (elements [ex0, ex1)); planes K*(ex0-1) .. K*ex1
+  int ex0 = 0, ex1 = 0, xs = 0, nplanes = 1, ecur = 0;
+  if (!xdeg) {
+    ex0 = a.ex_begin + chunk * a.xe_chunk;
+    ex1 = min(a.ex_end, ex0 + a.xe_chunk);
+    ecur = ex0 > 0 ? ex0 - 1 : 0;
+    xs = K * ecur;
+    nplanes = K * ex1 - xs + 1;
+  }
+
+  // ---- fixed per-thread work descriptors ----
+  const long long plane_stride = (long long)g.ny * g.nz;
+  // U-plane load items: slots outside the domain are zeroed once (in both buffers) and never
+  // loaded; in-domain slots get one 8-byte cp.async per plane (zero-fill only for constrained
+  // boundary nodes).
+  const double* lsrc[G::LIT];
+  unsigned ldst[G::LIT];
+  bool lbnd[G::LIT];
+#pragma unroll
+  for (int i = 0; i < G::LIT; ++i) {
+    const int idx = tid + i * NT;
+    lsrc[i] = nullptr;
+    ldst[i] = 0u;
+    lbnd[i] = false;
+    if (idx < G::LITEMS) {
+      const int q = idx / (NYin * NZin);
+      const int rem = idx - q * (NYin * NZin);
+      const int yy = rem / NZin, zz = rem - yy * NZin;
+      const int gy = y_lo - K + yy, gz = z_lo - K + zz;
+      const int slot = (q * NYin + yy) * NZp + zz;
+      if (gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz) {
+        ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
+        lsrc[i] = u + (long long)q * a.su + (long long)gy * g.nz + gz;
+        lbnd[i] = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
+      } else {
+        Us[slot] = 0.0;
+        Us[G::U_SZ + slot] = 0.0;
+      }
+    }
+  }
+  constexpr unsigned UBUF = G::U_SZ * sizeof(double);
+
+  auto load_plane = [&](int x, int buf) {
+    const long long xoff = (long long)x * plane_stride;
+    if (!a.constrained) {
+#pragma unroll
+      for (int i = 0; i < G::LIT; ++i) {
+        if (lsrc[i] == nullptr) continue;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ldst[i] + buf * UBUF),
+                     "l"(lsrc[i] + xoff) : "memory");
+      }
+    } else {
+      const bool xb = !xdeg && (x == 0 || x == g.nx - 1);
+#pragma unroll
+      for (int i = 0; i < G::LIT; ++i) {
+        if (lsrc[i] == nullptr) continue;
+        const int nb = (xb || lbnd[i]) ? 0 : 8;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
+                     "l"(lsrc[i] + xoff), "r"(nb) : "memory");
+      }
+    }
+    cp_async_commit();
+  };
+
+  // Z items: (q, yy, segment of ZS elements); lanes run along yy (odd pitch -> no bank conflicts)
+  int zoff[G::ZIT], zeb[G::ZIT];
+#pragma unroll
+  for (int i = 0; i < G::ZIT; ++i) {
+    const int it = tid + i * NT;
+    zeb[i] = TZE;  // inactive
+    zoff[i] = 0;
+    if (it < G::ZITEMS) {
+      const int yy = it % NYin;
+      const int rest = it / NYin;
+      const int seg = rest % G::ZSEG, q = rest / G::ZSEG;
+      if (!ydeg || yy == K) {
+        zeb[i] = seg * G::ZS;
+        zoff[i] = q * NYin + yy;  // row index
+      }
+    }
+  }
+  // Y items: (q, z, segment of YS elements); lanes run along z
+  int yoff[G::YIT], yeb[G::YIT];
+#pragma unroll
+  for (int i = 0; i < G::YIT; ++i) {
+    // Y items are placed on the threads with the fewest Z items (balance inside the interval)
+    constexpr int YOFF = (G::YITEMS % NT == 0) ? 0 : NT - (G::YITEMS % NT);
+    const int it = (tid + NT - YOFF) % NT + i * NT;
+    yeb[i] = TYE;
+    yoff[i] = 0;
+    if (it < G::YITEMS) {
+      const int zl = it % TZ;
+      const int rest = it / TZ;
+      const int seg = rest % G::YSEG, q = rest / G::YSEG;
+      if (zl < nzo) {
+        yeb[i] = seg * G::YS;
+        yoff[i] = q * 4096 + zl;  // packed (q, zl)
+      }
+    }
+  }
+
+  // ---------------- Z-phase: A = Mz u, B = Kz u ----------------
+  auto zphase = [&](int ub, int ab) {
+    const double* Ub = Us + ub * G::U_SZ;
+    double* As = ABs + ab * 2 * G::AB_SZ;
+    double* Bs = As + G::AB_SZ;
+#pragma unroll
+    for (int i = 0; i < G::ZIT; ++i) {
+      if (zeb[i] >= nez) continue;
+      const double* row = Ub + zoff[i] * NZp;
+      double* arow = As + zoff[i] * TZp;
+      double* brow = Bs + zoff[i] * TZp;
+      const int e_beg = zeb[i];
+      double L[K + 1], R[K + 1];
+#pragma unroll
+      for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
+#pragma unroll
+      for (int el = 0; el < G::ZS; ++el) {
+        const int e = e_beg + el;
+        if (e < nez) {
+          R[0] = L[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) R[s] = row[K * e + K + s];
+          const int ez = ez0 + e;
+          const double wl = ez > 0 ? 1.0 : 0.0, wr = ez < g.Ez ? 1.0 : 0.0;
+          double oa[K], ob[K];
+          elem2<K>(cf, L, R, wl, wr, oa, ob);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int zl = K * e + r;
+            arow[zl] = oa[r];  // zl < TZ always; columns >= nzo are never read
+            brow[zl] = ob[r];
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) L[s] = R[s];
+        }
+      }
+    }
+  };
+
+  // ---------------- Y-phase: MA = My A, C = Ky A + My B ----------------
+  auto yphase = [&](int ab, int mc) {
+    const double* As = ABs + ab * 2 * G::AB_SZ;
+    const double* Bs = As + G::AB_SZ;
+    double* MAs = MCs + mc * 2 * G::MC_SZ;
+    double* Cs = MAs + G::MC_SZ;
+    if (ydeg) {
+      for (int it = tid; it < Q * TZ; it += NT) {
+        const int q = it / TZ, zl = it - q * TZ;
+        if (zl < nzo) {
+          MAs[(q * TY) * TZp + zl] = As[(q * NYin + K) * TZp + zl];
+          Cs[(q * TY) * TZp + zl] = Bs[(q * NYin + K) * TZp + zl];
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < G::YIT; ++i) {
+      if (yeb[i] >= ney) continue;
+      const int q = yoff[i] >> 12, zl = yoff[i] & 4095;
+      const double* acol = As + (q * NYin) * TZp + zl;
+      const double* bcol = Bs + (q * NYin) * TZp + zl;
+      double* mcol = MAs + (q * TY) * TZp + zl;
+      double* ccol = Cs + (q * TY) * TZp + zl;
+      const int e_beg = yeb[i];
+      double La[K + 1], Ra[K + 1], Lb[K + 1], Rb[K + 1];
+#pragma unroll
+      for (int s = 0; s <= K; ++s) {
+        La[s] = acol[(K * e_beg + s) * TZp];
+        Lb[s] = bcol[(K * e_beg + s) * TZp];
+      }
+#pragma unroll
+      for (int el = 0; el < G::YS; ++el) {
+        const int e = e_beg + el;
+        if (e < ney) {
+          Ra[0] = La[K];
+          Rb[0] = Lb[K];
+#pragma unroll
+          for (int s = 1; s <= K; ++s) {
+            Ra[s] = acol[(K * e + K + s) * TZp];
+            Rb[s] = bcol[(K * e + K + s) * TZp];
+          }
+          const int ey = ey0 + e;
+          const double wl = ey > 0 ? 1.0 : 0.0, wr = ey < g.Ey ? 1.0 : 0.0;
+          double om[K], oc[K];
+          elem3<K>(cf, La, Ra, Lb, Rb, wl, wr, om, oc);
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int yl = K * e + r;  // yl < TY always; rows >= nyo are never read
+            mcol[yl * TZp] = om[r];
+            ccol[yl * TZp] = oc[r];
+          }
+#pragma unroll
+          for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
+        }
+      }
+    }
+  };
+
+  // X-phase state
+  double acc[PPT][Q][K + 1];
+  int pyl[PPT], pzl[PPT];
+  bool pv[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int p = tid + j * NT;
+    pyl[j] = p / TZ;
+    pzl[j] = p - pyl[j] * TZ;
+    pv[j] = (p < TY * TZ) && pyl[j] < nyo && pzl[j] < nzo;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) acc[j][q][s] = 0.0;
+  }
+  double sumsq = 0.0;
+  const bool dm_ident = a.dm_identity != 0;
+
+  // ---------------- X-phase: stage mix + element-push accumulation ----------------
+  // the plane's local index r within element ecur is uniform: dispatch to a copy with the x-table
+  // column as compile-time register operands
+  auto xphase_r = [&](auto RC, int x, int mc) {
+    constexpr int RR = decltype(RC)::value;
+    const double* MAs = MCs + mc * 2 * G::MC_SZ;
+    const double* Cs = MAs + G::MC_SZ;
+    constexpr int r_loc = RR;
+    double cmx[K + 1], ckx[K + 1];
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      cmx[s] = cf.m(s, RR);
+      ckx[s] = cf.s(s, RR);
+    }
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (!pv[j]) continue;
+      const int yl = pyl[j], zl = pzl[j];
+      double ma[Q], cc[Q], pq[Q], qq[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        ma[q] = MAs[(q * TY + yl) * TZp + zl];
+        cc[q] = Cs[(q * TY + yl) * TZp + zl];
+      }
+      if constexpr (BLOCK) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          pq[q] = fma(lamq[q], ma[q], a.tau * cc[q]);
+          qq[q] = a.tau * ma[q];
+        }
+      } else {
+        if (dm_ident) {  // D_M diagonal (the IRK operator I(x)M + tau A(x)K)
+#pragma unroll
+          for (int i = 0; i < Q; ++i) {
+            double p = a.DM[i][i] * ma[i], s2 = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < Q; ++jj) {
+              p = fma(a.DK[i][jj], cc[jj], p);
+              s2 = fma(a.DK[i][jj], ma[jj], s2);
+            }
+            pq[i] = p;
+            qq[i] = s2;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) {
+            double p = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < Q; ++jj) {
+              p = fma(a.DM[i][jj], ma[jj], p);
+              p = fma(a.DK[i][jj], cc[jj], p);
+              s2 = fma(a.DK[i][jj], ma[jj], s2);
+            }
+            pq[i] = p;
+            qq[i] = s2;
+          }
+        }
+      }
+      const int y = y_lo + yl, z = z_lo + zl;
+      if (xdeg) {
+        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, 0, y, z, pq, sumsq);
+        continue;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int s = 0; s <= K; ++s) acc[j][q][s] = fma(cmx[s], pq[q], fma(ckx[s], qq[q], acc[j][q][s]));
+      if (r_loc == K) {
+        // element ecur complete: nodes K*ecur + s, s < K
+        if (ecur >= ex0) {
+#pragma unroll
+          for (int s = 0; s < K; ++s) {
+            double val[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
+            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, K * ecur + s, y, z, val, sumsq);
+          }
+        }
+        if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
+          double val[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
+          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, K * g.Ex, y, z, val, sumsq);
+        }
+        // carry the shared vertex and start the next element with this plane as its local 0
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double carry = acc[j][q][K];
+#pragma unroll
+          for (int s = 0; s <= K; ++s) acc[j][q][s] = fma(cf.m(s, 0), pq[q], cf.s(s, 0) * qq[q]);
+          acc[j][q][0] += carry;
+        }
+      }
+    }
+    if (!xdeg && r_loc == K) ++ecur;
+  };
+  auto xphase = [&](int x, int mc) {
+    const int r_loc = xdeg ? 0 : x - K * ecur;   // 0..K
+    switch (r_loc) {
+      case 0: xphase_r(IC<0>{}, x, mc); break;
+      case 1: xphase_r(IC<1>{}, x, mc); break;
+      case 2: if constexpr (K >= 2) xphase_r(IC<2>{}, x, mc); break;
+      case 3: if constexpr (K >= 3) xphase_r(IC<3>{}, x, mc); break;
+      case 4: if constexpr (K >= 4) xphase_r(IC<4>{}, x, mc); break;
+    }
+  };
+
+  if constexpr (G::PIPE3) {
+    // Three-stage software pipeline, ONE barrier per plane: interval t runs Z(t), Y(t-1), X(t-2)
+    // on disjoint double buffers (U/AB/MC indexed by plane parity) while U(t+1) is in flight.
+    load_plane(xs, 0);
+    for (int t = 0; t < nplanes + 2; ++t) {
+      cp_async_wait_all();
+      __syncthreads();
+      if (t + 1 < nplanes) load_plane(xs + t + 1, (t + 1) & 1);
+      if (t < nplanes) zphase(t & 1, t & 1);
+      if (t >= 1 && t - 1 < nplanes) yphase((t - 1) & 1, (t - 1) & 1);
+      if (t >= 2) xphase(xs + t - 2, t & 1);
+    }
+  } else {
+    // Two barriers per plane: Z(x+1) and X(x) share an interval (U/AB vs MC), Y(x+1) follows.
+    load_plane(xs, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    zphase(0, 0);
+    if (nplanes > 1) load_plane(xs + 1, 1);
+    __syncthreads();
+    yphase(0, 0);
+    for (int pl = 0; pl < nplanes; ++pl) {
+      cp_async_wait_all();
+      __syncthreads();                     // U(x+1) landed; MC(x) ready; AB consumed
+      if (pl + 2 < nplanes) load_plane(xs + pl + 2, pl & 1);
+      if (pl + 1 < nplanes) zphase((pl + 1) & 1, 0);
+      xphase(xs + pl, 0);
+      __syncthreads();                     // AB(x+1) ready; MC(x) consumed
+      if (pl + 1 < nplanes) yphase(0, 0);
+    }
+  }
+
+  if constexpr (EPI == EPI_DINV) {
+    // deterministic per-CTA partial: fixed-shape tree in shared memory
+    __syncthreads();
+    double* red = smem;
+    red[tid] = sumsq;
+    __syncthreads();
+    for (int off = NT / 2; off > 0; off >>= 1) {
+      if (tid < off) red[tid] += red[tid + off];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      a.partial[cta] = red[0];
+    }
+  }
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
+  using G = Geo<K, Q>;
+  const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
+  static bool configured = false;
+  auto kern = stage_apply_kernel<K, Q, BLOCK, EPI>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int gz = (a.g.Ez + 1 + G::TZE - 1) / G::TZE;
+  const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + G::TYE - 1) / G::TYE;
+  const int nb = BLOCK ? a.nblk / Q : 1;  // CTA groups of Q blocks
+  dim3 grid(gz, gy, a.nchunks * nb);
+  if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
+  kern<<<grid, G::NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+#define SPK_EPIS(K, Q, B)                                                   \
+  switch (epi) {                                                            \
+    case EPI_STORE: return launch_one<K, Q, B, EPI_STORE>(a, s, n);         \
+    case EPI_RESID: return launch_one<K, Q, B, EPI_RESID>(a, s, n);         \
+    case EPI_CHEB: return launch_one<K, Q, B, EPI_CHEB>(a, s, n);           \
+    case EPI_DINV: return launch_one<K, Q, B, EPI_DINV>(a, s, n);           \
+  }                                                                         \
+  return cudaErrorInvalidValue;
+
+template <int K>
+cudaError_t dispatch_k(int Q, bool block_mode, int epi, const SpkApplyArgs& a, cudaStream_t s, int* n) {
+  if (block_mode) {  // Q = blocks per CTA (diagonal mix, per-block shifts)
+    switch (Q) {
+      case 1: SPK_EPIS(K, 1, true)
+      case 2: SPK_EPIS(K, 2, true)
+      case 3: SPK_EPIS(K, 3, true)
+      case 4: SPK_EPIS(K, 4, true)
+    }
+    return cudaErrorInvalidValue;
+  }
+  switch (Q) {
+    case 1: return launch_one<K, 1, false, EPI_STORE>(a, s, n);
+    case 2: SPK_EPIS(K, 2, false)
+    case 3: return launch_one<K, 3, false, EPI_STORE>(a, s, n);
+    case 4: return launch_one<K, 4, false, EPI_STORE>(a, s, n);
+  }
+  return cudaErrorInvalidValue;
+}
+#undef SPK_EPIS
+
+}  // namespace

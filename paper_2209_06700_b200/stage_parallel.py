@@ -1,0 +1,205 @@
+"""Stage-parallel Radau IIA step across GPUs (the paper's layout).
+
+Rank r of the stage communicator owns a contiguous group of stages (Q / world each; the mesh is not
+partitioned, B = 1), so every block solve of eq. irk:P runs locally with no inter-stage traffic.
+Only three kinds of exchange remain:
+
+* stage combines (D (x) I) u for D in {S~^-1, S~, A^-1}: a Cannon-like ring (`RingCombiner`): in round
+  s rank r holds the stage group of rank (r + s) mod world, adds D[own, held] @ held, and passes it on
+  (world - 1 shifts of one stage group; grouped isend/irecv, NCCL over NVLink on the GPU path);
+* GMRES inner products: local partial dot + all-reduce (fixed order, deterministic per run);
+* nothing else: the right-hand side and the update are stage-local.
+
+The driver is backend-agnostic: `backend` supplies the stage-local operators. `GPUStageBackend` uses
+the device kernels (K1 block mode, MultiBlockSolver, spk_rhs); tests/test_stage_parallel_gloo.py runs the
+same driver with a CPU backend built on the oracle over gloo and checks it against the single-process
+oracle stepper.
+"""
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .tableau import crout_lu, radau_iia, spectral_real
+
+
+def stage_groups(Q, world):
+    """Contiguous stage ranges per rank (as equal as possible)."""
+    base, extra = divmod(Q, world)
+    out, s = [], 0
+    for r in range(world):
+        c = base + (1 if r < extra else 0)
+        out.append((s, s + c))
+        s += c
+    return out
+
+
+class RingCombiner:
+    """v_own = sum_j D[own, j] x_j with x distributed by stage groups (Cannon-like rotation)."""
+
+    def __init__(self, groups, rank, world, group=None):
+        self.groups, self.rank, self.world, self.group = groups, rank, world, group
+        self.shift_rounds = 0
+
+    def __call__(self, D, x_local):
+        D = np.asarray(D)
+        r, W = self.rank, self.world
+        lo, hi = self.groups[r]
+        n = x_local.shape[-1]
+        out = torch.zeros((hi - lo, n), dtype=x_local.dtype, device=x_local.device)
+        held = x_local.contiguous()
+        held_owner = r
+        maxg = max(g[1] - g[0] for g in self.groups)
+        for s in range(W):
+            hlo, hhi = self.groups[held_owner]
+            blk = torch.from_numpy(np.ascontiguousarray(D[lo:hi, hlo:hhi])).to(x_local.device, x_local.dtype)
+            out.addmm_(blk, held[: hhi - hlo])
+            if s < W - 1:
+                send = torch.zeros((maxg, n), dtype=x_local.dtype, device=x_local.device)
+                send[: held.shape[0]] = held[: hhi - hlo]
+                recv = torch.empty_like(send)
+                ops = [dist.P2POp(dist.isend, send, self.groups_rank((r - 1) % W), self.group),
+                       dist.P2POp(dist.irecv, recv, self.groups_rank((r + 1) % W), self.group)]
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+                held = recv
+                held_owner = (held_owner + 1) % W
+                self.shift_rounds += 1
+        return out
+
+    def groups_rank(self, r):
+        return r  # ranks of the stage communicator are 0..world-1 in the default group
+
+
+class DistKrylov:
+    """Right-preconditioned MGS GMRES (krylov.py:28-103 semantics) with all-reduced inner products."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def dot(self, a, b):
+        t = torch.sum(a * b).reshape(1).to(torch.float64)
+        dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+    def solve(self, A, P, b, rel_tol=1e-12, max_iter=200):
+        beta = np.sqrt(self.dot(b, b))
+        hist = [beta]
+        if beta == 0.0:
+            return torch.zeros_like(b), 0, hist, True
+        target = rel_tol * beta
+        V = [b / beta]
+        H = np.zeros((max_iter + 1, max_iter))
+        g = np.zeros(max_iter + 1)
+        g[0] = beta
+        k, happy = 0, False
+        for j in range(max_iter):
+            w = A(P(V[j]))
+            for i in range(j + 1):
+                H[i, j] = self.dot(V[i], w)
+                w = w - H[i, j] * V[i]
+            H[j + 1, j] = np.sqrt(self.dot(w, w))
+            if not np.all(np.isfinite(H[: j + 2, j])):
+                raise FloatingPointError("non-finite GMRES value")
+            k = j + 1
+            if abs(H[j + 1, j]) < 1e-30:
+                happy = True
+            else:
+                V.append(w / H[j + 1, j])
+            y, *_ = np.linalg.lstsq(H[: k + 1, :k], g[: k + 1], rcond=None)
+            res = float(np.linalg.norm(g[: k + 1] - H[: k + 1, :k] @ y))
+            hist.append(res)
+            if happy or res <= target:
+                break
+        y, *_ = np.linalg.lstsq(H[: k + 1, :k], g[: k + 1], rcond=None)
+        z = torch.zeros_like(b)
+        for i in range(k):
+            z = z + float(y[i]) * V[i]
+        x = P(z)
+        r = b - A(x)
+        true_res = np.sqrt(self.dot(r, r))
+        conv = happy or true_res <= target * (1 + 1e-9) or hist[-1] <= target
+        return x, k, hist, conv
+
+
+class StageParallelStepper:
+    """eq. irk:A solved by GMRES with the eq. irk:P preconditioner, stages distributed over ranks."""
+
+    def __init__(self, backend, Q, tau, rank, world, group=None, tableau=None, rel_tol=1e-12, max_iter=200):
+        self.be, self.Q, self.tau = backend, Q, float(tau)
+        self.rank, self.world = rank, world
+        self.rel_tol, self.max_iter = rel_tol, max_iter
+        tab = tableau if tableau is not None else radau_iia(Q)
+        get = lambda t, k: np.asarray(t[k] if isinstance(t, dict) else getattr(t, k))
+        self.A, self.b, self.c, self.Ainv = get(tab, "A"), get(tab, "b"), get(tab, "c"), get(tab, "Ainv")
+        sp = spectral_real(crout_lu(self.Ainv).L)
+        self.lams, self.S, self.Sinv = sp.lambdas, sp.S, sp.Sinv
+        self.groups = stage_groups(Q, world)
+        self.lo, self.hi = self.groups[rank]
+        self.ring = RingCombiner(self.groups, rank, world, group)
+        self.kry = DistKrylov(group)
+        backend.setup(self.lams[self.lo : self.hi], self.tau)
+
+    def A_op(self, k):
+        """mask (Ainv M (mask k) + tau K (mask k)) + (1 - mask) k, own stages."""
+        mk, kk = self.be.mass_stiff(k)
+        v = self.ring(self.Ainv, mk) + self.tau * kk
+        return self.be.boundary_identity(v, k)
+
+    def P_op(self, r):
+        w = self.ring(self.Sinv, r)
+        z = self.be.vcycle(w)
+        return self.ring(self.S, z)
+
+    def step(self, t_n, u_n):
+        w = self.be.stage_rhs(t_n, u_n, self.c[self.lo : self.hi] * self.tau)  # (own, n): F_j - K u_n
+        rhs = self.be.mask(self.ring(self.Ainv, w))
+        k, its, hist, conv = self.kry.solve(self.A_op, self.P_op, rhs, self.rel_tol, self.max_iter)
+        # u_{n+1} = u_n + tau sum_i b_i k_i: partial sum over own stages, all-reduced
+        part = self.tau * torch.einsum("i,in->n", torch.as_tensor(self.b[self.lo : self.hi], dtype=k.dtype,
+                                                                  device=k.device), k)
+        dist.all_reduce(part, group=self.kry.group)
+        return u_n + part, its, conv
+
+
+class GPUStageBackend:
+    """Stage-local device operators for StageParallelStepper (one GPU per rank)."""
+
+    def __init__(self, hierarchy, config=None, source=None):
+        from .fem import SeparableSolution
+        from .multigrid import VCycleConfig
+
+        self.h = hierarchy
+        self.L = hierarchy.max_level
+        self.config = config or VCycleConfig()
+        self.source = source or SeparableSolution(hierarchy.dim)
+
+    def setup(self, lams, tau):
+        from .multigrid import MultiBlockSolver
+
+        self.tau = tau
+        self.solver = MultiBlockSolver(self.h, lams, tau, self.config) if len(lams) else None
+        self.g1 = torch.from_numpy(self.h.load_vector_1d(self.L, self.source.s)).to(self.h.device)
+        self.maskt = self.h.mask_tensor(self.L)
+
+    def mass_stiff(self, k):
+        km = torch.where(self.maskt, k, torch.zeros_like(k))
+        return (self.h.apply_block(self.L, 1.0, 0.0, km), self.h.apply_block(self.L, 0.0, 1.0, km))
+
+    def boundary_identity(self, v, k):
+        return torch.where(self.maskt, v, k)
+
+    def mask(self, v):
+        return torch.where(self.maskt, v, torch.zeros_like(v))
+
+    def vcycle(self, w):
+        return self.solver.apply_device(w.contiguous(), check=False)
+
+    def stage_rhs(self, t_n, u_n, ctau):
+        um = torch.where(self.maskt, u_n, torch.zeros_like(u_n)).reshape(1, -1)
+        ku = self.h.apply_block(self.L, 0.0, 1.0, um)[0]
+        fhat = torch.empty_like(u_n)
+        from . import _lib
+        from ._device import ptr, stream_ptr
+        _lib.call("spk_outer3", self.h.ctx, self.L, ptr(self.g1), ptr(fhat), stream_ptr(self.h.device))
+        return torch.stack([self.source.F(t_n + ct) * fhat - ku for ct in ctau])

@@ -199,3 +199,29 @@ def test_real_and_complex_paths_agree(cuda):
     ua, _, _ = a.run(3)
     ub, _, _ = b.run(3)
     assert rel(ub.cpu().numpy(), ua.cpu().numpy()) < 1e-8
+
+
+def test_stage_parallel_gpu_backend_single_rank(cuda):
+    """GPUStageBackend + StageParallelStepper on one rank (NCCL world of 1) == StageSystem."""
+    import os
+    import torch.distributed as dist
+    from paper_2209_06700_b200.stage_parallel import GPUStageBackend, StageParallelStepper
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        h = build_hierarchy(3, 3, 2)
+        tab = ref_radau(3)
+        cfg = VCycleConfig(smoother_degree=3)
+        sp = StageParallelStepper(GPUStageBackend(h, cfg), 3, 0.01, 0, 1, tableau=tab)
+        ss = StageSystem(h, 3, 0.01, config=cfg, tableau=tab)
+        u1 = ss.initial_condition()
+        u2 = u1.clone()
+        for s in range(2):
+            u1, rep = ss.step(s * 0.01, u1)
+            u2, its, conv = sp.step(s * 0.01, u2)
+            assert abs(its - rep.iterations) <= 1 and conv
+        assert rel(u2.cpu().numpy(), u1.cpu().numpy()) < 1e-9
+    finally:
+        dist.destroy_process_group()

@@ -1,0 +1,105 @@
+"""Stage-parallel stepper (stage groups over ranks, ring combines, all-reduced GMRES dots) on CPU
+with gloo, against the single-process oracle stepper."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleStageBackend:
+    """Stage-local operators from the CPU oracle (test double of GPUStageBackend)."""
+
+    def __init__(self, dim, L, k, deg):
+        from oracle.fem_qk import Hierarchy
+        from oracle.stepper import Separable
+
+        self.h = Hierarchy(dim, L, k)
+        self.L, self.deg = L, deg
+        self.src = Separable(dim)
+        self.mask_np = self.h.levels[L].interior_mask
+
+    def setup(self, lams, tau):
+        from oracle import solvers
+
+        self.tau = tau
+        self.vc = solvers.VCycle(self.h, lams, tau, solvers.Config(smoother_degree=self.deg))
+        self.m = torch.from_numpy(self.mask_np)
+
+    def mass_stiff(self, k):
+        km = np.where(self.mask_np, k.numpy(), 0.0)
+        return (torch.from_numpy(self.h.apply_mass(self.L, km)), torch.from_numpy(self.h.apply_stiffness(self.L, km)))
+
+    def boundary_identity(self, v, k):
+        return torch.where(self.m, v, k)
+
+    def mask(self, v):
+        return torch.where(self.m, v, torch.zeros_like(v))
+
+    def vcycle(self, w):
+        return torch.from_numpy(self.vc.apply(w.numpy()))
+
+    def stage_rhs(self, t_n, u_n, ctau):
+        ku = self.h.apply_stiffness(self.L, np.where(self.mask_np, u_n.numpy(), 0.0))
+        return torch.from_numpy(np.stack([self.h.load_vector(self.L, self.src.f, t_n + ct) - ku for ct in ctau]))
+
+
+def _worker(rank, world, port, Q, q_out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.tableau_ref import radau_iia
+        from paper_2209_06700_b200.stage_parallel import StageParallelStepper
+
+        be = OracleStageBackend(3, 3, 1, 5)
+        tab = radau_iia(Q)
+        sp = StageParallelStepper(be, Q, 0.05, rank, world, tableau=tab)
+        u = torch.from_numpy(be.src.u(be.h.node_coords(be.L), 0.0))
+        its = []
+        for s in range(2):
+            u, k, conv = sp.step(s * 0.05, u)
+            its.append(k)
+        if rank == 0:
+            q_out.put((u.numpy(), its, sp.ring.shift_rounds))
+    except Exception as e:  # pragma: no cover
+        q_out.put(repr(e))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Q,world", [(2, 2), (3, 2), (4, 2)])
+def test_stage_parallel_matches_oracle(Q, world):
+    from oracle import stepper
+    from oracle.fem_qk import Hierarchy
+    from oracle.tableau_ref import radau_iia
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, Q, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    res = q.get()
+    assert not isinstance(res, str), res
+    u_dist, its_dist, shifts = res
+    ref = stepper.RealLU(Hierarchy(3, 3, 1), Q, 0.05, tab=radau_iia(Q))
+    u = ref.initial()
+    its = []
+    for i in range(2):
+        u, k, _ = ref.step(i * 0.05, u)
+        its.append(k)
+    assert all(abs(a - b) <= 1 for a, b in zip(its_dist, its)), (its_dist, its)
+    assert np.abs(u_dist - u).max() / np.abs(u).max() < 1e-9
+    # (world - 1) ring shifts per combine, 3 combines per GMRES iteration (+ 1 for the RHS, the final
+    # P^-1 and A) -> strictly positive and a multiple of world - 1
+    assert shifts > 0 and shifts % (world - 1) == 0
