@@ -77,15 +77,17 @@ int spk_residual(spk_ctx* ctx, int level, int nblk, const double* lams, double t
                  const double* b, double* r, double* d_out, const double* c2s, void* stream);
 int spk_cheb_init(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* cs,
                   const double* b, double* r, double* x, double* d, void* stream);
+/* final_step != 0: fused last step, writes only x <- x + d_in + d_new and raises *nan_flag on NaN/Inf */
 int spk_cheb_step(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* c1s,
                   const double* c2s, const double* d_in, double* r, double* x, double* d_out,
-                  void* stream);
+                  int final_step, int* nan_flag, void* stream);
 int spk_pair_residual(spk_ctx* ctx, int level, double re, double im, double tau, const double* x,
                       const double* b, double* r, double* d_out, double c2, void* stream);
 int spk_pair_cheb_init(spk_ctx* ctx, int level, double re, double im, double tau, double c,
                        const double* b, double* r, double* x, double* d, void* stream);
 int spk_pair_cheb_step(spk_ctx* ctx, int level, double re, double im, double tau, double c1, double c2,
-                       const double* d_in, double* r, double* x, double* d_out, void* stream);
+                       const double* d_in, double* r, double* x, double* d_out, int final_step,
+                       int* nan_flag, void* stream);
 /* power iteration step: w = Dinv A u, *norm_dev = ||w||_2 (device scalar); pair != 0 uses (re, im) */
 int spk_dinv_norm(spk_ctx* ctx, int level, int pair, double lam_or_re, double im, double tau,
                   const double* u, double* w, double* norm_dev, void* stream);

@@ -46,12 +46,12 @@ _SIGS = {
     "spk_pair_apply": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_int, c_vp, c_vp, c_vp], c_int),
     "spk_residual": ([c_vp, c_int, c_int, P_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, P_dbl, c_vp], c_int),
     "spk_cheb_init": ([c_vp, c_int, c_int, P_dbl, c_dbl, P_dbl, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
-    "spk_cheb_step": ([c_vp, c_int, c_int, P_dbl, c_dbl, P_dbl, P_dbl, c_vp, c_vp, c_vp, c_vp, c_vp],
-                      c_int),
+    "spk_cheb_step": ([c_vp, c_int, c_int, P_dbl, c_dbl, P_dbl, P_dbl, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                       c_vp], c_int),
     "spk_pair_residual": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp], c_int),
     "spk_pair_cheb_init": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
-    "spk_pair_cheb_step": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp],
-                           c_int),
+    "spk_pair_cheb_step": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_int,
+                            c_vp, c_vp], c_int),
     "spk_dinv_norm": ([c_vp, c_int, c_int, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_transfer": ([c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_vp], c_int),
     "spk_axpy_flag": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),

@@ -139,7 +139,9 @@ void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb) {
   if (a.g.Ex == 0) { a.nchunks = 1; a.xe_chunk = 1; a.ex_begin = 0; a.ex_end = 0; return; }
   if (a.ex_end <= a.ex_begin) { a.ex_begin = 0; a.ex_end = a.g.Ex; }
   const int nel = a.ex_end - a.ex_begin;
-  const long long target = c->target_ctas > 0 ? c->target_ctas : 2 * 148 * 2;
+  // ~4 waves of one CTA per SM: fewer, longer x-chunks amortise the one-element chunk halo
+  // (C2 is flat between 4 and 6 waves; C4's block-mode sweeps prefer 4, tools/prof_apply.py)
+  const long long target = c->target_ctas > 0 ? c->target_ctas : 4 * 148;
   long long nch = (target + tiles - 1) / tiles;
   if (nch < 1) nch = 1;
   if (nch > nel) nch = nel;
@@ -445,11 +447,12 @@ int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double ta
 
 int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
                   const double* c2s, const double* d_in, double* r, double* x, double* d_out,
-                  void* stream) {
+                  int final_step, int* nan_flag, void* stream) {
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs a = base_args(c, level);
   a.u = d_in; a.su = n; a.r = r; a.x = x; a.d_out = d_out; a.se = n;
+  a.final_step = final_step; a.nan_flag = nan_flag;
   return apply_blocks_chunked(c, level, nblk, lams, 0, tau, 1, EPI_CHEB, a, (cudaStream_t)stream, c1s,
                               c2s);
 }
@@ -484,11 +487,13 @@ int spk_pair_cheb_init(spk_ctx* c, int level, double re, double im, double tau, 
 }
 
 int spk_pair_cheb_step(spk_ctx* c, int level, double re, double im, double tau, double c1, double c2,
-                       const double* d_in, double* r, double* x, double* d_out, void* stream) {
+                       const double* d_in, double* r, double* x, double* d_out, int final_step,
+                       int* nan_flag, void* stream) {
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs a = base_args(c, level);
   a.u = d_in; a.su = n; a.r = r; a.x = x; a.d_out = d_out; a.se = n;
+  a.final_step = final_step; a.nan_flag = nan_flag;
   a.constrained = 1;
   a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
   a.DK[0][0] = tau; a.DK[1][1] = tau;

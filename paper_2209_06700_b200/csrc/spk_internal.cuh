@@ -64,6 +64,8 @@ struct SpkApplyArgs {
   double jre, jim;
   double* partial;        // EPI_DINV: per-CTA partial sums (deterministic reduction)
   double hd, hk;          // host only: h^dim and h^(dim-2) folded into the mix by the launcher
+  int final_step;         // EPI_CHEB: last step -> write x + d_new only (fused x + d), NaN flag
+  int* nan_flag;
 };
 
 // launchers (stage_apply.cu)

@@ -47,12 +47,20 @@ template <int K, int Q> struct Geo {
   static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ;
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
+#ifdef SPK_ZS
+  static constexpr int ZS = (Q >= 2) ? SPK_ZS : 1;
+#else
   static constexpr int ZS = 1;
+#endif
   static constexpr int ZSEG = (TZE + ZS - 1) / ZS;
   static constexpr int ZITEMS = Q * NYin * ZSEG;
   static constexpr int ZIT = (ZITEMS + NT - 1) / NT;
   // Y items: (q, z, element segment)
+#ifdef SPK_YS
+  static constexpr int YS = (Q >= 2) ? SPK_YS : 1;
+#else
   static constexpr int YS = 1;
+#endif
   static constexpr int YSEG = (TYE + YS - 1) / YS;
   static constexpr int YITEMS = Q * TZ * YSEG;
   static constexpr int YIT = (YITEMS + NT - 1) / NT;
@@ -258,7 +266,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
         sumsq = fma(z0[q], z0[q], sumsq);
       }
     } else {
-      double rn[Q];
+      double rn[Q], xfin[Q];
       if constexpr (EPI == EPI_RESID) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -270,12 +278,18 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
         for (int q = 0; q < Q; ++q) {
           const double dq = __ldg(a.u + ubase + q * a.su + gi);
           rn[q] = a.r[ebase + q * a.se + gi] - Av[q];
-          a.r[ebase + q * a.se + gi] = rn[q];
-          a.x[ebase + q * a.se + gi] = a.x[ebase + q * a.se + gi] + dq;
+          const double xq = a.x[ebase + q * a.se + gi] + dq;
+          if (!a.final_step) {
+            a.r[ebase + q * a.se + gi] = rn[q];
+            a.x[ebase + q * a.se + gi] = xq;
+          } else {
+            xfin[q] = xq;
+          }
         }
       }
       if (a.d_out != nullptr) {
         jacobi(rn);
+        bool bad = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int slot = BLOCK ? slot0 + q : 0;
@@ -283,11 +297,18 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
           if constexpr (EPI == EPI_CHEB) {
             const double dq = __ldg(a.u + ubase + q * a.su + gi);
             dn = a.c1[slot] * dq + a.c2[slot] * z0[q];
+            if (a.final_step) {  // last step fused with "return x + d" (multigrid.py:88) + NaN check
+              const double xn = xfin[q] + dn;
+              a.x[ebase + q * a.se + gi] = xn;
+              bad |= !isfinite(xn);
+              continue;
+            }
           } else {
             dn = z0[q] / a.c2[slot];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
           }
           a.d_out[ebase + q * a.se + gi] = dn;
         }
+        if (bad && a.nan_flag) atomicOr(a.nan_flag, 1);
       }
     }
   }

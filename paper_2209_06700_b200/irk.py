@@ -71,6 +71,8 @@ class StageSystem:
         if isinstance(self.source, SeparableSolution):
             self._g1 = torch.from_numpy(hierarchy.load_vector_1d(self.level, self.source.s)).to(dev)
         self.vcycles = 0
+        self.use_graphs = True
+        self._graph = None
 
     # ---- pieces ----
     def assemble_rhs(self, t_n, u_n):
@@ -93,11 +95,29 @@ class StageSystem:
     def apply_system_operator(self, k):
         return self.h.apply_stage_operator(self.level, self.Ainv, self.tau * np.eye(self.Q), k, constrained=True)
 
-    def apply_preconditioner(self, r):
+    def _precond_body(self, r, out):
         w = dense_combine(self.Sinv, r.reshape(self.Q, self.n), hierarchy=self.h)
         z = self.precond.apply_device(w, check=False)
+        return dense_combine(self.S, z, out=out, hierarchy=self.h)
+
+    def apply_preconditioner(self, r):
+        """P^-1 r: combine(S~^-1) -> Q V-cycles -> combine(S~). The whole chain (tens of small
+        launches per level) is captured once as a CUDA graph and replayed."""
         self.vcycles += 1
-        return dense_combine(self.S, z, hierarchy=self.h)
+        if not self.use_graphs:
+            return self._precond_body(r, None)
+        if self._graph is None:
+            self._g_in = torch.zeros((self.Q, self.n), dtype=torch.float64, device=self.h.device)
+            self._g_out = torch.zeros_like(self._g_in)
+            self._precond_body(self._g_in, self._g_out)  # warm-up: configures kernels, allocates
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._precond_body(self._g_in, self._g_out)
+            self._graph = g
+        self._g_in.copy_(r.reshape(self.Q, self.n))
+        self._graph.replay()
+        return self._g_out
 
     def step(self, t_n, u_n, check=True):
         """u_{n+1} for device u_n (n,), and the SolveReport."""

@@ -178,20 +178,23 @@ class _DeviceVCycle:
                 _lib.call("spk_residual", h.ctx, level, nb, lams, self.tau, ptr(lv.x), ptr(b), ptr(lv.r),
                           ptr(lv.d), thetas, st)
         deg = self.config.smoother_degree
-        if deg > 1:
-            coefs = [sm.coefficients() for sm in sms]
-            for k in range(deg - 1):
-                if self.pair:
-                    c1, c2 = coefs[0][k]
-                    _lib.call("spk_pair_cheb_step", h.ctx, level, self.re_lam, self.im_lam, self.tau, c1, c2,
-                              ptr(lv.d), ptr(lv.r), ptr(lv.x), ptr(lv.d2), st)
-                else:
-                    c1s = _lib.dbl_array([c[k][0] for c in coefs])
-                    c2s = _lib.dbl_array([c[k][1] for c in coefs])
-                    _lib.call("spk_cheb_step", h.ctx, level, self.nrows, _lib.dbl_array(self._block_lams()),
-                              self.tau, c1s, c2s, ptr(lv.d), ptr(lv.r), ptr(lv.x), ptr(lv.d2), st)
-                lv.d, lv.d2 = lv.d2, lv.d
-        _lib.call("spk_axpy_flag", lv.x.numel(), ptr(lv.x), ptr(lv.d), ptr(self._flags[level:]), st)
+        flag = ptr(self._flags[level:])
+        if deg == 1:
+            _lib.call("spk_axpy_flag", lv.x.numel(), ptr(lv.x), ptr(lv.d), flag, st)
+            return
+        coefs = [sm.coefficients() for sm in sms]
+        for k in range(deg - 1):
+            final = 1 if k == deg - 2 else 0  # last step also performs "return x + d" (fused)
+            if self.pair:
+                c1, c2 = coefs[0][k]
+                _lib.call("spk_pair_cheb_step", h.ctx, level, self.re_lam, self.im_lam, self.tau, c1, c2,
+                          ptr(lv.d), ptr(lv.r), ptr(lv.x), ptr(lv.d2), final, flag, st)
+            else:
+                c1s = _lib.dbl_array([c[k][0] for c in coefs])
+                c2s = _lib.dbl_array([c[k][1] for c in coefs])
+                _lib.call("spk_cheb_step", h.ctx, level, self.nrows, _lib.dbl_array(self._block_lams()),
+                          self.tau, c1s, c2s, ptr(lv.d), ptr(lv.r), ptr(lv.x), ptr(lv.d2), final, flag, st)
+            lv.d, lv.d2 = lv.d2, lv.d
 
     def _residual_restrict(self, level, b, lv):
         h = self.hierarchy
