@@ -44,7 +44,10 @@ template <int K, int Q> struct Geo {
   static constexpr int U_SZ = Q * NYin * NZp;          // one plane buffer
   static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
   static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
-  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ;
+  // Jacobi table: one entry per (x,y,z) node class ((K+1)^3) and block (block mode) / (A, B) (pair)
+  static constexpr int DT_STRIDE = (Q > 2 ? Q : 2);
+  static constexpr int DT_SZ = (K + 1) * (K + 1) * (K + 1) * DT_STRIDE;
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ + DT_SZ;
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
 #ifdef SPK_ZS
@@ -156,6 +159,30 @@ __device__ __forceinline__ void node_diag(const SpkDims& g, int x, int y, int z,
   dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
 }
 
+// Node class along one axis for the Jacobi table: 0 interior vertex, 1..K-1 element-interior node,
+// K boundary vertex (the assembled 1D diagonal takes K+1 distinct values). Degenerate axis: 0.
+template <int K>
+__device__ __forceinline__ int axis_class(int i, int n, int E) {
+  if (E == 0) return 0;
+  const int r = i % K;
+  if (r != 0) return r;
+  return (i == 0 || i == n - 1) ? K : 0;
+}
+
+template <int K>
+__device__ __forceinline__ void class_diag1(int c, int E, double& dm, double& dk) {
+  using H = Hat<K>;
+  if (E == 0) { dm = 1.0; dk = 0.0; return; }
+  if (c == 0) { dm = H::M(K, K) + H::M(0, 0); dk = H::S(K, K) + H::S(0, 0); return; }
+  if (c == K) { dm = H::M(0, 0); dk = H::S(0, 0); return; }
+  double m = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int rr = 1; rr < K; ++rr)
+    if (rr == c) { m = H::M(rr, rr); s2 = H::S(rr, rr); }
+  dm = m;
+  dk = s2;
+}
+
 __device__ __forceinline__ bool on_boundary(const SpkDims& g, int x, int y, int z) {
   return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
          (g.Ez > 0 && (z == 0 || z == g.nz - 1));
@@ -224,8 +251,9 @@ __device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 
 // Fused epilogue at one node for all Q stages / blocks of the CTA. Block mode: stage q of the CTA is
 // block b0 + q with its own shift lam[q] (and Chebyshev coefficients in its parameter slot).
 template <int K, int Q, bool BLOCK, int EPI>
-__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q], int x, int y,
-                                         int z, const double (&val)[Q], double& sumsq) {
+__device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q],
+                                         const double* dtab, const double (&ith)[Q], int x, int y, int z,
+                                         const double (&val)[Q], double& sumsq) {
   const SpkDims& g = a.g;
   const long long gi = ((long long)x * g.ny + y) * g.nz + z;
   const bool bnd = a.constrained && on_boundary(g, x, y, z);
@@ -241,19 +269,19 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
 #pragma unroll
     for (int q = 0; q < Q; ++q) __stcs(a.v + vbase + q * a.sv + gi, Av[q]);
   } else {
-    // Jacobi diagonal (analytic; reference operator_diagonal fem.py:172-187, 1.0 on boundary)
-    double dm, dk;
-    node_diag<K>(g, x, y, z, dm, dk);
+    // Jacobi diagonal (reference operator_diagonal fem.py:172-187, 1.0 on boundary): looked up in
+    // the per-CTA table of node classes (no per-node division)
+    constexpr int K1 = K + 1;
+    const int cls = (axis_class<K>(x, g.nx, g.Ex) * K1 + axis_class<K>(y, g.ny, g.Ey)) * K1 +
+                    axis_class<K>(z, g.nz, g.Ez);
+    const double* dt = dtab + cls * Geo<K, Q>::DT_STRIDE;
     double z0[Q];  // Dinv applied to the quantity of the epilogue
     auto jacobi = [&](const double (&rr)[Q]) {
       if constexpr (BLOCK) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) z0[q] = (bnd ? 1.0 : 1.0 / (lamq[q] * dm + a.tau * dk)) * rr[q];
+        for (int q = 0; q < Q; ++q) z0[q] = (bnd ? 1.0 : dt[q]) * rr[q];
       } else {  // pair 2x2 block Jacobi (multigrid.py:268-276, 306-313)
-        const double da = bnd ? 1.0 : a.jre * dm + a.tau * dk;
-        const double db = bnd ? 0.0 : a.jim * dm;
-        const double det = da * da + db * db;
-        const double A_ = da / det, B_ = db / det;
+        const double A_ = bnd ? 1.0 : dt[0], B_ = bnd ? 0.0 : dt[1];
         z0[0] = A_ * rr[0] + B_ * rr[1];
         if constexpr (Q > 1) z0[1] = -B_ * rr[0] + A_ * rr[1];
       }
@@ -304,7 +332,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
               continue;
             }
           } else {
-            dn = z0[q] / a.c2[slot];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
+            dn = z0[q] * ith[q];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
           }
           a.d_out[ebase + q * a.se + gi] = dn;
         }
@@ -326,6 +354,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
   double* Us = smem;                    // [2][Q][NYin][NZp]
   double* ABs = Us + 2 * G::U_SZ;       // [2][A|B][Q][NYin][TZp]
   double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][MA|C][Q][TY][TZp]
+  double* dtab = MCs + 2 * G::NBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
 
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
@@ -344,6 +373,31 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
   double lamq[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) lamq[q] = BLOCK ? (a.lam_uniform ? a.lam[0] : a.lam[b0 - a.blk_base + q]) : 0.0;
+  double ith[Q];  // 1 / theta per block (post-smoothing start)
+#pragma unroll
+  for (int q = 0; q < Q; ++q) ith[q] = 1.0 / a.c2[BLOCK ? b0 - a.blk_base + q : 0];
+  if constexpr (EPI != EPI_STORE) {
+    constexpr int K1 = K + 1;
+    for (int idx = tid; idx < K1 * K1 * K1; idx += NT) {
+      const int cx = idx / (K1 * K1), cy = (idx / K1) % K1, cz = idx % K1;
+      double mx, kx, my, ky, mz, kz;
+      class_diag1<K>(cx, g.Ex, mx, kx);
+      class_diag1<K>(cy, g.Ey, my, ky);
+      class_diag1<K>(cz, g.Ez, mz, kz);
+      const double dm = (mx * my) * mz;
+      const double dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+      double* e = dtab + idx * G::DT_STRIDE;
+      if constexpr (BLOCK) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) e[q] = 1.0 / (lamq[q] * dm + a.tau * dk);
+      } else {
+        const double da = a.jre * dm + a.tau * dk, db = a.jim * dm;
+        const double det = da * da + db * db;
+        e[0] = da / det;
+        e[1] = db / det;
+      }
+    }
+  }
 
   // reference-element tables in registers (distinct entries only)
   Coef<K> cf;
@@ -626,7 +680,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
       }
       const int y = y_lo + yl, z = z_lo + zl;
       if (xdeg) {
-        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, 0, y, z, pq, sumsq);
+        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, 0, y, z, pq, sumsq);
         continue;
       }
 #pragma unroll
@@ -641,14 +695,14 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, Geo<K, Q>::MINB)
             double val[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
-            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, K * ecur + s, y, z, val, sumsq);
+            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * ecur + s, y, z, val, sumsq);
           }
         }
         if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
           double val[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
-          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, K * g.Ex, y, z, val, sumsq);
+          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * g.Ex, y, z, val, sumsq);
         }
         // carry the shared vertex and start the next element with this plane as its local 0
 #pragma unroll

@@ -211,21 +211,42 @@ __device__ void finalize_partials(double mine, double* partial, unsigned* counte
 }
 
 // ---- MGS step: w -= h_prev * v_prev ; out = <v_cur, w> (or ||w|| if v_cur == null) ----
-__global__ void mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
+__global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
+  // 4 independent elements per thread and iteration keep enough loads in flight to stream HBM
   __shared__ double red[TPB];
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   const double h = a.v_prev ? *a.h_prev : 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long i = base;
+  for (; i + 3 * stride < a.n; i += 4 * stride) {
+    double w[4], c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = a.w[i + u * stride];
+    if (a.v_prev) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w[u] = w[u] - h * a.v_prev[i + u * stride];
+        a.w[i + u * stride] = w[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = a.v_cur ? a.v_cur[i + u * stride] : w[u];
+    s0 = fma(c[0], w[0], s0);
+    s1 = fma(c[1], w[1], s1);
+    s2 = fma(c[2], w[2], s2);
+    s3 = fma(c[3], w[3], s3);
+  }
+  for (; i < a.n; i += stride) {
     double w = a.w[i];
     if (a.v_prev) {
       w = w - h * a.v_prev[i];
       a.w[i] = w;
     }
     const double c = a.v_cur ? a.v_cur[i] : w;
-    s = fma(c, w, s);
+    s0 = fma(c, w, s0);
   }
-  const double mine = block_sum(s, red);
+  const double mine = block_sum((s0 + s1) + (s2 + s3), red);
   finalize_partials(mine, a.partial, a.counter, a.out, a.v_cur == nullptr, red);
 }
 
@@ -364,7 +385,7 @@ cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-int spk_mgs_grid() { return 148 * 2; }
+int spk_mgs_grid() { return 148 * 8; }
 
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s) {
   mgs_kernel<<<spk_mgs_grid(), TPB, 0, s>>>(a);
