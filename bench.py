@@ -138,10 +138,16 @@ def run_ours(args):
     from paper_2209_06700_b200.tableau import radau_iia
 
     rank, world, local = dist_env()
+    if os.environ.get("BENCH_SHARE_GPU"):  # functional multi-rank test on one GPU (gloo only)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     Q, k, tau, L = CFG["Q"], CFG["degree"], CFG["tau"], args.level
     hier = build_hierarchy(3, L, k, device=dev)
     n = hier.levels[L].n_dofs
@@ -150,9 +156,17 @@ def run_ours(args):
     rng = np.random.default_rng(CFG["seed"] + rank)
     u_host = torch.from_numpy(rng.uniform(-1.0, 1.0, size=(Q, n))).pin_memory()
     v_host = torch.empty_like(u_host).pin_memory()
-    u = u_host.to(dev)
-    v = torch.empty_like(u)
     op = SlabOperator(hier, L, DM, DK, world=world, rank=rank) if world > 1 else None
+    if op is None:
+        u = u_host.to(dev)
+        v = torch.empty_like(u)
+    else:
+        # slab buffers: [k halo planes | owned planes | 1 halo plane]; this rank's 64^3-cell block
+        # fills the owned planes (the last rank also owns the global boundary plane)
+        u, v = op.alloc()
+        lay = op.layout
+        own = lay.owned_slice()
+        u[:, own] = u_host[:, : own.stop - own.start].to(dev)
 
     def apply_dev():
         if op is None:
@@ -186,7 +200,10 @@ def run_ours(args):
     # ---- kernel-only time of K1 (single launch, same stream) ----
     kern_ms = []
     for _ in range(5):
-        kern_ms.append(measure.event_time(lambda: hier.apply_stage_operator(L, DM, DK, u, out=v)))
+        if op is None:
+            kern_ms.append(measure.event_time(lambda: hier.apply_stage_operator(L, DM, DK, u, out=v)))
+        else:
+            kern_ms.append(measure.event_time(lambda: op.launch(u, v)))
     kern_ms = sorted(kern_ms)[len(kern_ms) // 2]
     peak, peak_kind = measure.measured_peaks()
     alg_bytes = 16.0 * Q * n
@@ -218,9 +235,13 @@ def run_ours(args):
     else:
         e2.record(s)
         for _ in range(args.steps):
-            u.copy_(u_host, non_blocking=True)
+            own = op.layout.owned_slice()
+            m = own.stop - own.start
+            for q in range(Q):
+                u[q, own].copy_(u_host[q, :m], non_blocking=True)
             apply_dev()
-            v_host.copy_(v, non_blocking=True)
+            for q in range(Q):
+                v_host[q, :m].copy_(v[q, own], non_blocking=True)
         e3.record(s)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3) / args.steps

@@ -56,20 +56,23 @@ def exchange_halo(buf, layout, group=None):
     ops = []
     recv_bufs = []
     Q = buf.shape[0]
+    # gloo moves host memory only: stage device halos through the host (functional testing)
+    host = buf.is_cuda and dist.get_backend(group) == "gloo"
+    wire = (lambda t: t.cpu()) if host else (lambda t: t.contiguous())
     for q in range(Q):
         row = buf[q]
         if r + 1 < W:
             send = row[layout.plane_slice(k + k * E - k, k + k * E)]
-            ops.append(dist.P2POp(dist.isend, send.contiguous(), r + 1, group))
+            ops.append(dist.P2POp(dist.isend, wire(send), r + 1, group))
             rv = row[layout.plane_slice(k + k * E, k + k * E + 1)]
-            tmp = torch.empty_like(rv)
+            tmp = torch.empty_like(rv, device="cpu" if host else rv.device)
             recv_bufs.append((rv, tmp))
             ops.append(dist.P2POp(dist.irecv, tmp, r + 1, group))
         if r > 0:
             send = row[layout.plane_slice(k, k + 1)]
-            ops.append(dist.P2POp(dist.isend, send.contiguous(), r - 1, group))
+            ops.append(dist.P2POp(dist.isend, wire(send), r - 1, group))
             lv = row[layout.plane_slice(0, k)]
-            tmp = torch.empty_like(lv)
+            tmp = torch.empty_like(lv, device="cpu" if host else lv.device)
             recv_bufs.append((lv, tmp))
             ops.append(dist.P2POp(dist.irecv, tmp, r - 1, group))
     if ops:
@@ -103,8 +106,12 @@ class SlabOperator:
                 torch.zeros((self.Q, n), dtype=torch.float64, device=self.hier.device))
 
     def apply(self, u, v):
+        exchange_halo(u, self.layout, self.group)
+        return self.launch(u, v)
+
+    def launch(self, u, v):
+        """The windowed K1 launch alone (halos already in place)."""
         lay = self.layout
-        exchange_halo(u, lay, self.group)
         n = lay.local_numel
         if self.rank == 0:
             base_u = u[:, lay.plane_slice(self.k, lay.nplanes)]
