@@ -41,19 +41,24 @@ class RingCombiner:
         self.groups, self.rank, self.world, self.group = groups, rank, world, group
         self.shift_rounds = 0
 
-    def __call__(self, D, x_local):
+    def __call__(self, D, x_local, in_groups=None, out_groups=None):
+        """in_groups / out_groups: row ranges of D's columns / rows owned by each rank (default:
+        the stage groups for both)."""
         D = np.asarray(D)
+        ig = in_groups or self.groups
+        og = out_groups or self.groups
         r, W = self.rank, self.world
-        lo, hi = self.groups[r]
+        lo, hi = og[r]
         n = x_local.shape[-1]
         out = torch.zeros((hi - lo, n), dtype=x_local.dtype, device=x_local.device)
         held = x_local.contiguous()
         held_owner = r
-        maxg = max(g[1] - g[0] for g in self.groups)
+        maxg = max(max(g[1] - g[0] for g in ig), 1)
         for s in range(W):
-            hlo, hhi = self.groups[held_owner]
+            hlo, hhi = ig[held_owner]
             blk = torch.from_numpy(np.ascontiguousarray(D[lo:hi, hlo:hhi])).to(x_local.device, x_local.dtype)
-            out.addmm_(blk, held[: hhi - hlo])
+            if hhi > hlo and hi > lo:
+                out.addmm_(blk, held[: hhi - hlo])
             if s < W - 1:
                 send = torch.zeros((maxg, n), dtype=x_local.dtype, device=x_local.device)
                 send[: held.shape[0]] = held[: hhi - hlo]
@@ -203,3 +208,108 @@ class GPUStageBackend:
         from ._device import ptr, stream_ptr
         _lib.call("spk_outer3", self.h.ctx, self.L, ptr(self.g1), ptr(fhat), stream_ptr(self.h.device))
         return torch.stack([self.source.F(t_n + ct) * fhat - ku for ct in ctau])
+
+
+class DirectComplexParallelStepper:
+    """eq. irk:Ainv with the conjugate-pair blocks distributed over ranks (SPEC complex_solver
+    stage-pair parallelism): w = S^-1 rhs and k = S z are ring combines between the stage groups and
+    the pair groups; each rank solves its own pair blocks (GMRES on the real 2x2 form with PRESB or
+    the 2x2 GMG V-cycle; the odd-Q real eigenvalue with the plain V-cycle) with no further traffic."""
+
+    def __init__(self, backend, Q, tau, rank, world, group=None, tableau=None, variant="presb",
+                 rel_tol=1e-12, max_iter=200):
+        from .tableau import spectral_complex
+        from .tensor_ops import paired_back_matrix, paired_forward_matrix
+
+        self.be, self.Q, self.tau, self.rank, self.world = backend, Q, float(tau), rank, world
+        self.rel_tol, self.max_iter = rel_tol, max_iter
+        tab = tableau if tableau is not None else radau_iia(Q)
+        get = lambda t, k: np.asarray(t[k] if isinstance(t, dict) else getattr(t, k))
+        self.b, self.c, self.Ainv = get(tab, "b"), get(tab, "c"), get(tab, "Ainv")
+        sp = spectral_complex(self.Ainv)
+        self.pairs = sp.pairs
+        self.Wf = paired_forward_matrix(sp.Sinv, sp.pairs)
+        self.Wb = paired_back_matrix(sp.S, sp.pairs)
+        P = len(sp.pairs)
+        self.groups = stage_groups(Q, world)
+        pg = stage_groups(P, world)
+        self.pair_groups = pg
+        self.row_groups = [(2 * a, 2 * b) for a, b in pg]
+        self.lo, self.hi = self.groups[rank]
+        self.ring = RingCombiner(self.groups, rank, world, group)
+        self.group = group
+        own = [self.pairs[i] for i in range(*pg[rank])]
+        backend.setup_pairs(own, self.tau, variant)
+
+    def step(self, t_n, u_n):
+        w = self.be.stage_rhs(t_n, u_n, self.c[self.lo : self.hi] * self.tau)
+        rhs = self.be.mask(self.ring(self.Ainv, w))
+        wp = self.ring(self.Wf, rhs, in_groups=self.groups, out_groups=self.row_groups)
+        z = torch.zeros_like(wp)
+        its = []
+        for i in range(wp.shape[0] // 2):
+            zi, k = self.be.solve_pair(i, wp[2 * i : 2 * i + 2])
+            z[2 * i : 2 * i + 2] = zi
+            its.append(k)
+        kst = self.ring(self.Wb, z, in_groups=self.row_groups, out_groups=self.groups)
+        part = self.tau * torch.einsum("i,in->n", torch.as_tensor(self.b[self.lo : self.hi], dtype=kst.dtype,
+                                                                  device=kst.device), kst)
+        dist.all_reduce(part, group=self.group)
+        return u_n + part, its
+
+
+def _gpu_setup_pairs(self, own_pairs, tau, variant):
+    """Pair-block solvers for DirectComplexParallelStepper (GPUStageBackend extension)."""
+    from .multigrid import BlockSolver, PairBlockSolver
+
+    self.tau = tau
+    self.g1 = torch.from_numpy(self.h.load_vector_1d(self.L, self.source.s)).to(self.h.device)
+    self.maskt = self.h.mask_tensor(self.L)
+    self.pair_blocks = []
+    for p in own_pairs:
+        if p.is_real:
+            self.pair_blocks.append(("real", p, BlockSolver(self.h, p.re, tau, self.config)))
+        elif variant == "presb":
+            self.pair_blocks.append(("presb", p, BlockSolver(self.h, p.re + p.im, tau, self.config)))
+        else:
+            self.pair_blocks.append(("gmg", p, PairBlockSolver(self.h, p.re, p.im, tau, self.config)))
+
+
+def _gpu_solve_pair(self, i, rows):
+    """GMRES on the real 2x2 form of pair block i (rows: (2, n) re/im right-hand side)."""
+    from . import _lib
+    from ._device import ptr, stream_ptr
+    from .krylov import gmres
+
+    kind, p, vc = self.pair_blocks[i]
+    h, L = self.h, self.L
+    if kind == "real":
+        op = lambda v: h.apply_block(L, p.re, self.tau, v.reshape(1, -1), constrained=True).reshape(v.shape)
+        pc = lambda v: vc.apply_device(v.reshape(1, -1), check=False).reshape(v.shape)
+        z, rep = gmres(op, pc, rows[0].contiguous(), self.rel_tol, self.max_iter)
+        out = torch.zeros_like(rows)
+        out[0] = z
+        return out, rep.iterations
+
+    def op(v):
+        v = v.contiguous()
+        w = torch.empty_like(v)
+        _lib.call("spk_pair_apply", h.ctx, L, p.re, p.im, self.tau, 1, ptr(v), ptr(w), stream_ptr(h.device))
+        return w
+
+    if kind == "presb":
+        def pc(r):
+            y1 = vc.apply_device((r[0] + r[1]).reshape(1, -1), check=False)
+            y2 = vc.apply_device(r[1].reshape(1, -1) - h.apply_block(L, p.im, 0.0, y1, constrained=True),
+                                 check=False)
+            return torch.cat([y1 - y2, y2], dim=0)
+    else:
+        pc = lambda r: vc.apply_device(r.contiguous(), check=False)
+    z, rep = gmres(op, pc, rows.contiguous(), self.rel_tol, self.max_iter)
+    return z, rep.iterations
+
+
+GPUStageBackend.setup_pairs = _gpu_setup_pairs
+GPUStageBackend.solve_pair = _gpu_solve_pair
+GPUStageBackend.rel_tol = 1e-12
+GPUStageBackend.max_iter = 200

@@ -225,3 +225,26 @@ def test_stage_parallel_gpu_backend_single_rank(cuda):
         assert rel(u2.cpu().numpy(), u1.cpu().numpy()) < 1e-9
     finally:
         dist.destroy_process_group()
+
+
+def test_direct_complex_parallel_gpu_backend_single_rank(cuda):
+    import os
+    import torch.distributed as dist
+    from paper_2209_06700_b200.stage_parallel import DirectComplexParallelStepper, GPUStageBackend
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29534"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        h = build_hierarchy(3, 2, 3)
+        tab = ref_radau(3)
+        sp = DirectComplexParallelStepper(GPUStageBackend(h), 3, 5e-3, 0, 1, tableau=tab, variant="presb")
+        ds = DirectComplexSystem(h, 3, 5e-3, variant="presb", tableau=tab)
+        u1 = ds.initial_condition()
+        u2 = u1.clone()
+        for s in range(2):
+            u1, rep = ds.step(s * 5e-3, u1)
+            u2, its = sp.step(s * 5e-3, u2)
+        assert rel(u2.cpu().numpy(), u1.cpu().numpy()) < 1e-9
+    finally:
+        dist.destroy_process_group()

@@ -103,3 +103,98 @@ def test_stage_parallel_matches_oracle(Q, world):
     # (world - 1) ring shifts per combine, 3 combines per GMRES iteration (+ 1 for the RHS, the final
     # P^-1 and A) -> strictly positive and a multiple of world - 1
     assert shifts > 0 and shifts % (world - 1) == 0
+
+
+class OracleComplexBackend(OracleStageBackend):
+    def setup_pairs(self, own_pairs, tau, variant):
+        from oracle import solvers
+
+        self.tau = tau
+        self.m = torch.from_numpy(self.mask_np)
+        cfg = solvers.Config(smoother_degree=self.deg)
+        self.blocks = []
+        for p in own_pairs:
+            if p.is_real:
+                self.blocks.append(("real", p, solvers.VCycle(self.h, [p.re], tau, cfg)))
+            elif variant == "presb":
+                self.blocks.append(("presb", p, solvers.VCycle(self.h, [p.re + p.im], tau, cfg)))
+            else:
+                self.blocks.append(("gmg", p, solvers.VCycle(self.h, tau=tau, cfg=cfg, pair=(p.re, p.im))))
+
+    def solve_pair(self, i, rows):
+        from oracle import solvers
+
+        kind, p, vc = self.blocks[i]
+        h, L, tau = self.h, self.L, self.tau
+        r = rows.numpy()
+        if kind == "real":
+            z, its, _, _ = solvers.gmres(lambda v: h.apply_constrained(L, p.re, tau, v), vc.apply, r[0])
+            out = np.zeros_like(r)
+            out[0] = z
+            return torch.from_numpy(out), its
+
+        def op(u):
+            ui = np.where(self.mask_np, u, 0.0)
+            mr, mi = h.apply_mass(L, ui[0]), h.apply_mass(L, ui[1])
+            kr, ki = h.apply_stiffness(L, ui[0]), h.apply_stiffness(L, ui[1])
+            out = np.stack([p.re * mr + tau * kr - p.im * mi, p.im * mr + p.re * mi + tau * ki])
+            return np.where(self.mask_np, out, u)
+
+        if kind == "presb":
+            def pc(v):
+                y1 = vc.apply(v[0] + v[1])
+                y2 = vc.apply(v[1] - h.apply_constrained(L, p.im, 0.0, y1))
+                return np.stack([y1 - y2, y2])
+        else:
+            pc = vc.apply
+        z, its, _, _ = solvers.gmres(op, pc, r)
+        return torch.from_numpy(z), its
+
+
+def _cworker(rank, world, port, Q, variant, q_out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.tableau_ref import radau_iia
+        from paper_2209_06700_b200.stage_parallel import DirectComplexParallelStepper
+
+        be = OracleComplexBackend(3, 2, 2, 3)
+        sp = DirectComplexParallelStepper(be, Q, 5e-3, rank, world, tableau=radau_iia(Q), variant=variant)
+        u = torch.from_numpy(be.src.u(be.h.node_coords(be.L), 0.0))
+        for s in range(2):
+            u, its = sp.step(s * 5e-3, u)
+        if rank == 0:
+            q_out.put(u.numpy())
+    except Exception as e:  # pragma: no cover
+        q_out.put(repr(e))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Q,variant", [(3, "presb"), (4, "gmg")])
+def test_direct_complex_parallel_matches_oracle(Q, variant):
+    from oracle import solvers, stepper
+    from oracle.fem_qk import Hierarchy
+    from oracle.tableau_ref import radau_iia
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    procs = [ctx.Process(target=_cworker, args=(r, world, port, Q, variant, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    res = q.get()
+    assert not isinstance(res, str), res
+    ref = stepper.DirectComplex(Hierarchy(3, 2, 2), Q, 5e-3, variant, solvers.Config(smoother_degree=3),
+                                tab=radau_iia(Q))
+    u = ref.initial()
+    for i in range(2):
+        u, _ = ref.step(i * 5e-3, u)
+    assert np.abs(res - u).max() / np.abs(u).max() < 1e-9
