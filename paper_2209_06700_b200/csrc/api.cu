@@ -132,7 +132,7 @@ int ensure_scratch(spk_ctx* c, int need) {
 
 // x-chunking of the sliding window: enough CTAs to fill every SM about twice
 void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb) {
-  static const int TYE[5] = {0, 16, 8, 5, 4}, TZE[5] = {0, 32, 16, 11, 8};
+  static const int TYE[5] = {0, 16, 8, 5, 4}, TZE[5] = {0, 16, 8, 5, 4};  // = Tile<K> (stage_apply.cuh)
   const int gz = (a.g.Ez + 1 + TZE[K] - 1) / TZE[K];
   const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + TYE[K] - 1) / TYE[K];
   const long long tiles = (long long)gz * gy * nb;
