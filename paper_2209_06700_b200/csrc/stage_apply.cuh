@@ -478,9 +478,21 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, (EPI == EPI_STORE || Q <= 2) ? 
     zeb[i] = TZE;  // inactive
     zoff[i] = 0;
     if (it < G::ZITEMS) {
-      const int yy = it % NYin;
-      const int rest = it / NYin;
-      const int seg = rest % G::ZSEG, q = rest / G::ZSEG;
+      // item order: first rows 0..15 of every (q, segment) -- whole half-warps on one segment, so
+      // the odd row pitch makes them conflict-free -- then the remaining rows, row-major across
+      // (q, segment) (the mixed half-warps that remain are conflict-free for these pitches too)
+      constexpr int R = NYin < 16 ? NYin : 16;
+      constexpr int QS = Q * G::ZSEG;
+      int yy, qs;
+      if (it < QS * R) {
+        qs = it / R;
+        yy = it - qs * R;
+      } else {
+        const int idx = it - QS * R;
+        yy = R + idx / QS;
+        qs = idx - (yy - R) * QS;
+      }
+      const int seg = qs % G::ZSEG, q = qs / G::ZSEG;
       if (!ydeg || yy == K) {
         zeb[i] = seg * G::ZS;
         zoff[i] = q * NYin + yy;  // row index
