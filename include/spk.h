@@ -23,6 +23,8 @@
  *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
  *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
  *   spk_mask                GridHierarchy.constrain                       fem.py:153-158
+ *   spk_ctx_set_slab        (no reference code: the paper's spatial partition inside a stage
+ *                           group; SPEC RankGrid partitions b)
  */
 #ifndef SPK_H_
 #define SPK_H_
@@ -48,6 +50,14 @@ const char* spk_last_error(void);
 /* host-side discretisation data (no GPU needed) */
 int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out);
 int spk_ctx_destroy(spk_ctx* ctx);
+/* Turn level `level` of a 3D context into an x-slab window of the global 2^level-element mesh:
+ * the local arrays hold x_elems elements along x (K*x_elems+1 planes) whose plane 0 is global
+ * plane x0_plane (negative on the first slab: padding planes); every entry point at this level then
+ * produces only the nodes of local elements [ex_begin, ex_end) (+ the last vertex plane if
+ * store_last), with boundary rows, Jacobi classes and sources taken at global x positions.
+ * Halo planes are the caller's (exchanged before each operator application). */
+int spk_ctx_set_slab(spk_ctx* ctx, int level, int x_elems, int x0_plane, int ex_begin, int ex_end,
+                     int store_last);
 int spk_level_info(const spk_ctx* ctx, int level, int* n_per_axis, long long* n_dofs, double* h,
                    int* n_elems);
 int spk_level_tables(const spk_ctx* ctx, int level, double* Me, double* Ke);

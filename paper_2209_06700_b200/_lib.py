@@ -31,6 +31,7 @@ _SIGS = {
     "spk_last_error": ([], ctypes.c_char_p),
     "spk_ctx_create": ([c_int, c_int, c_int, ctypes.POINTER(c_vp)], c_int),
     "spk_ctx_destroy": ([c_vp], c_int),
+    "spk_ctx_set_slab": ([c_vp, c_int, c_int, c_int, c_int, c_int, c_int], c_int),
     "spk_level_info": ([c_vp, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_ll), P_dbl,
                         ctypes.POINTER(c_int)], c_int),
     "spk_level_tables": ([c_vp, c_int, P_dbl, P_dbl], c_int),

@@ -15,6 +15,9 @@ struct spk_ctx {
   std::vector<SpkDims> dims;
   std::vector<SpkTab> tabs;
   std::vector<double> h;
+  // per-level x-slab window (spk_ctx_set_slab): nodes of elements [ex_begin, ex_end) (+ the last
+  // vertex plane if store_last) are produced; a whole-mesh level produces everything
+  std::vector<int> ex_begin, ex_end, store_last;
   double xi[SPK_KMAX + 1];
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
   int target_ctas = 0;    // 0: automatic x-chunking
@@ -156,7 +159,9 @@ SpkApplyArgs base_args(const spk_ctx* c, int level) {
   std::memset(&a, 0, sizeof(a));
   a.g = c->dims[level];
   a.t = c->tabs[level];
-  a.store_last = 1;
+  a.ex_begin = c->ex_begin[level];
+  a.ex_end = c->ex_end[level];
+  a.store_last = c->store_last[level];
   a.hd = std::pow(c->h[level], c->dim);
   a.hk = std::pow(c->h[level], c->dim - 2);
   return a;
@@ -277,6 +282,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
     g.ny = dim >= 2 ? nax : 1; g.Ey = dim >= 2 ? N : 0;
     g.nx = dim >= 3 ? nax : 1; g.Ex = dim >= 3 ? N : 0;
     g.n = (long long)g.nx * g.ny * g.nz;
+    g.x0 = 0; g.nxg = g.nx; g.Exg = g.Ex;
     const double h = 1.0 / N;
     SpkTab t;
     std::memset(&t, 0, sizeof(t));
@@ -288,6 +294,9 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
     c->dims.push_back(g);
     c->tabs.push_back(t);
     c->h.push_back(h);
+    c->ex_begin.push_back(0);
+    c->ex_end.push_back(g.Ex);
+    c->store_last.push_back(1);
   }
   *out = c;
   return SPK_OK;
@@ -298,6 +307,27 @@ int spk_ctx_destroy(spk_ctx* c) {
   if (c->partial) cudaFree(c->partial);
   if (c->counter) cudaFree(c->counter);
   delete c;
+  return SPK_OK;
+}
+
+int spk_ctx_set_slab(spk_ctx* c, int level, int x_elems, int x0_plane, int ex_begin, int ex_end,
+                     int store_last) {
+  if (int rc = check_level(c, level)) return rc;
+  if (c->dim != 3) return fail(SPK_ECONFIG, "slab windows need a 3D hierarchy");
+  SpkDims& g = c->dims[level];
+  const int Eg = 1 << level;
+  if (x_elems < 1 || ex_begin < 0 || ex_end > x_elems || ex_begin >= ex_end || x0_plane % c->K != 0 ||
+      x0_plane / c->K + ex_begin < 0 || x0_plane / c->K + ex_end > Eg)
+    return fail(SPK_ECONFIG, "bad slab window at level " + std::to_string(level));
+  g.Ex = x_elems;
+  g.nx = c->K * x_elems + 1;
+  g.n = (long long)g.nx * g.ny * g.nz;
+  g.x0 = x0_plane;
+  g.Exg = Eg;
+  g.nxg = c->K * Eg + 1;
+  c->ex_begin[level] = ex_begin;
+  c->ex_end[level] = ex_end;
+  c->store_last[level] = store_last;
   return SPK_OK;
 }
 
@@ -540,25 +570,24 @@ int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in,
   const SpkDims gf = c->dims[level], gc = c->dims[level - 1];
   const int nf = gf.nz, nc = gc.nz, Nc = gc.Ez;
   const int dim = c->dim;
-  // sweep order z (last axis), y, x; arrays are [nblk][x][y][z]
-  // current shape (per block): sizes along (x, y, z)
-  int sx = prolong ? (dim >= 3 ? nc : 1) : (dim >= 3 ? nf : 1);
+  // sweep order z (last axis), y, x; arrays are [nblk][x][y][z]; along x the levels may be slab
+  // windows (local planes, global offsets x0; only the owned output planes are produced)
+  int sx = prolong ? (dim >= 3 ? gc.nx : 1) : (dim >= 3 ? gf.nx : 1);
   int sy = prolong ? (dim >= 2 ? nc : 1) : (dim >= 2 ? nf : 1);
   int sz = prolong ? nc : nf;
   const int tz = prolong ? nf : nc;
-  const long long out_scratch_max = (long long)nblk * (long long)nf * nf * (dim >= 3 ? nf : 1);
-  (void)out_scratch_max;
-  // scratch holds two ping-pong intermediates
+  // scratch holds two ping-pong intermediates of at most nblk * max(local fine, local coarse) DoFs
+  const long long half = (long long)nblk * (gf.n > gc.n ? gf.n : gc.n);
   double* bufA = scratch;
-  double* bufB = scratch + (long long)nblk * (dim >= 3 ? (long long)nf * nf * nf : (long long)nf * nf);
+  double* bufB = scratch + half;
   const double* src = in;
   SpkTransferArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.Nc = Nc;
   a.prolong = prolong;
   for (int f = 0; f <= 2 * c->K; ++f)
     for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
   const SpkDims gout = prolong ? gf : gc;
+  const int lout = prolong ? level : level - 1;
   int nsweeps = dim;
   for (int sw = 0; sw < nsweeps; ++sw) {
     const bool last = (sw == nsweeps - 1);
@@ -568,17 +597,25 @@ int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in,
     a.accumulate = last ? accumulate : 0;
     a.mask = last ? mask : 0;
     a.g = gout;
+    a.Nc = Nc;
+    a.in_off = 0; a.out_off = 0; a.o_begin = 0;
     if (sw == 0) {  // z axis
-      a.outer = (long long)nblk * sx * sy; a.inner = 1; a.nin = sz; a.nout = tz;
+      a.outer = (long long)nblk * sx * sy; a.inner = 1; a.nin = sz; a.nout = tz; a.onodes = tz;
       sz = tz;
     } else if (sw == 1) {  // y axis
       const int ty = prolong ? nf : nc;
-      a.outer = (long long)nblk * sx; a.inner = sz; a.nin = sy; a.nout = ty;
+      a.outer = (long long)nblk * sx; a.inner = sz; a.nin = sy; a.nout = ty; a.onodes = ty;
       sy = ty;
-    } else {  // x axis
-      const int tx = prolong ? nf : nc;
-      a.outer = nblk; a.inner = (long long)sy * sz; a.nin = sx; a.nout = tx;
-      sx = tx;
+    } else {  // x axis: windowed
+      const SpkDims gi = prolong ? gc : gf;
+      a.Nc = gc.Exg;
+      a.outer = nblk; a.inner = (long long)sy * sz; a.nin = sx;
+      a.in_off = gi.x0; a.out_off = gout.x0;
+      a.onodes = gout.nx;
+      a.o_begin = c->K * c->ex_begin[lout];
+      a.nout = c->K * (c->ex_end[lout] - c->ex_begin[lout]) +
+               ((c->store_last[lout] && c->ex_end[lout] == gout.Ex) ? 1 : 0);
+      sx = gout.nx;
     }
     cudaError_t e = spk_launch_transfer(c->K, a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "transfer");

@@ -17,6 +17,10 @@ struct SpkDims {
   int nx, ny, nz;   // nodes per axis (1 for a degenerate axis)
   int Ex, Ey, Ez;   // elements per axis (0 for a degenerate axis)
   long long n;      // nx*ny*nz
+  // x-slab windows (mesh partition along x): local plane 0 is global plane x0 (may be negative:
+  // padding planes of the first slab); the global mesh has nxg planes / Exg elements along x.
+  // A whole-mesh level has x0 = 0, nxg = nx, Exg = Ex.
+  int x0, nxg, Exg;
 };
 
 // 1D element tables of one level, scaled by h (mass) and 1/h (stiffness), and the per-node

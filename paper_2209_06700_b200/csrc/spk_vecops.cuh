@@ -22,7 +22,10 @@ struct SpkTransferArgs {
   double* out;
   long long outer, inner;
   int nin, nout;
-  int Nc;         // coarse elements along the axis
+  int Nc;         // coarse elements along the axis (global)
+  int in_off, out_off;  // global node index of local node 0 of input / output along the axis
+  int o_begin;    // first local output node produced (nout nodes from there)
+  int onodes;     // local output nodes along the axis (extent of the output array)
   int prolong;    // 1: coarse -> fine, 0: restriction (transpose)
   int accumulate; // out += result
   int mask;       // zero boundary nodes of level g (final sweep)

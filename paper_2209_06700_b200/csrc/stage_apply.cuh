@@ -187,7 +187,7 @@ __device__ __forceinline__ void class_diag1(int c, int E, double& dm, double& dk
 }
 
 __device__ __forceinline__ bool on_boundary(const SpkDims& g, int x, int y, int z) {
-  return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+  return (g.Ex > 0 && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
          (g.Ez > 0 && (z == 0 || z == g.nz - 1));
 }
 
@@ -275,7 +275,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
     // Jacobi diagonal (reference operator_diagonal fem.py:172-187, 1.0 on boundary): looked up in
     // the per-CTA table of node classes (no per-node division)
     constexpr int K1 = K + 1;
-    const int cls = (axis_class<K>(x, g.nx, g.Ex) * K1 + axis_class<K>(y, g.ny, g.Ey)) * K1 +
+    const int cls = (axis_class<K>(x + g.x0, g.nxg, g.Ex) * K1 + axis_class<K>(y, g.ny, g.Ey)) * K1 +
                     axis_class<K>(z, g.nz, g.Ez);
     const double* dt = dtab + cls * Geo<K, Q>::DT_STRIDE;
     double z0[Q];  // Dinv applied to the quantity of the epilogue
@@ -411,7 +411,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, (EPI == EPI_STORE || Q <= 2) ? 
   if (!xdeg) {
     ex0 = a.ex_begin + chunk * a.xe_chunk;
     ex1 = min(a.ex_end, ex0 + a.xe_chunk);
-    ecur = ex0 > 0 ? ex0 - 1 : 0;
+    // first real element of the window (a first slab has padding planes x0 < 0 in front)
+    const int efirst = g.x0 < 0 ? -g.x0 / K : 0;
+    ecur = ex0 > efirst ? ex0 - 1 : ex0;
     xs = K * ecur;
     nplanes = K * ex1 - xs + 1;
   }
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, (EPI == EPI_STORE || Q <= 2) ? 
                      "l"(lsrc[i] + xoff) : "memory");
       }
     } else {
-      const bool xb = !xdeg && (x == 0 || x == g.nx - 1);
+      const bool xb = !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
 #pragma unroll
       for (int i = 0; i < G::LIT; ++i) {
         if (lsrc[i] == nullptr) continue;

@@ -33,8 +33,10 @@ __device__ __forceinline__ void decompose(long long gi, const SpkDims& g, int& x
   x = (int)(t / g.ny);
 }
 
+// boundary of the global mesh; nodes outside it (padding planes of a first / last slab window)
+// count as boundary (identity rows, zero sources)
 __device__ __forceinline__ bool bnd3(const SpkDims& g, int x, int y, int z) {
-  return (g.Ex > 0 && (x == 0 || x == g.nx - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+  return (g.Ex > 0 && (x + g.x0 <= 0 || x + g.x0 >= g.nxg - 1)) || (g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
          (g.Ez > 0 && (z == 0 || z == g.nz - 1));
 }
 
@@ -42,7 +44,7 @@ template <int K>
 __device__ __forceinline__ void nodediag(const SpkVecArgs& a, int x, int y, int z, double& dm,
                                          double& dk) {
   double mx, kx, my, ky, mz, kz;
-  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], x, a.g.Ex, mx, kx);
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], x + a.g.x0, a.g.Exg, mx, kx);
   dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], y, a.g.Ey, my, ky);
   dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], z, a.g.Ez, mz, kz);
   dm = (mx * my) * mz;
@@ -61,8 +63,8 @@ __global__ void cheb_init_kernel(const __grid_constant__ SpkVecArgs a) {
     int x, y, z;
     decompose(gi, a.g, x, y, z);
     const bool bnd = a.constrained && bnd3(a.g, x, y, z);
-    double dm, dk;
-    nodediag<K>(a, x, y, z, dm, dk);
+    double dm = 1.0, dk = 0.0;
+    if (!bnd) nodediag<K>(a, x, y, z, dm, dk);
     if (!a.pair) {
       const int slot = b - a.blk_base;
       const double lam = a.lam_uniform ? a.lam[0] : a.lam[slot];
@@ -107,9 +109,11 @@ __global__ void transfer_axis_kernel(const __grid_constant__ SpkTransferArgs a) 
        gid += (long long)gridDim.x * blockDim.x) {
     const long long in_idx = gid % a.inner;
     const long long rest = gid / a.inner;
-    const int i = (int)(rest % a.nout);
+    const int il = a.o_begin + (int)(rest % a.nout);  // local output node
+    const int i = il + a.out_off;                      // global output node
     const long long o = rest / a.nout;
-    const double* src = a.in + o * (long long)a.nin * a.inner + in_idx;
+    // input rows are addressed by global node index (local = global - in_off)
+    const double* src = a.in + o * (long long)a.nin * a.inner + in_idx - (long long)a.in_off * a.inner;
     double val = 0.0;
     if (a.prolong) {
       // fine node i <- coarse element ec, local fine position f in [0, 2K]
@@ -141,7 +145,7 @@ __global__ void transfer_axis_kernel(const __grid_constant__ SpkTransferArgs a) 
       }
     }
     (void)P2;
-    const long long oidx = (o * a.nout + i) * a.inner + in_idx;
+    const long long oidx = (o * (long long)a.onodes + il) * a.inner + in_idx;
     if (a.mask) {
       const long long gi = oidx % a.g.n;
       int x, y, z;
@@ -287,7 +291,8 @@ __global__ void outer3_kernel(const __grid_constant__ SpkSepArgs a) {
        i += (long long)gridDim.x * blockDim.x) {
     int x, y, z;
     decompose(i, a.g, x, y, z);
-    const double gx = a.g.Ex ? a.gx[x] : 1.0;
+    const int xg = x + a.g.x0;
+    const double gx = a.g.Ex ? ((xg >= 0 && xg < a.g.nxg) ? a.gx[xg] : 0.0) : 1.0;
     const double gy = a.g.Ey ? a.gx[y] : 1.0;
     a.out[i] = (gx * gy) * a.gx[z];
   }
@@ -300,7 +305,8 @@ __global__ void rhs_kernel(const __grid_constant__ SpkRhsArgs a) {
        i += (long long)gridDim.x * blockDim.x) {
     int x, y, z;
     decompose(i, a.g, x, y, z);
-    const double gx = a.g.Ex ? a.gx[x] : 1.0;
+    const int xg = x + a.g.x0;
+    const double gx = a.g.Ex ? ((xg >= 0 && xg < a.g.nxg) ? a.gx[xg] : 0.0) : 1.0;
     const double gy = a.g.Ey ? a.gx[y] : 1.0;
     const double fhat = (gx * gy) * a.gx[z];
     const double ku = a.ku[i];

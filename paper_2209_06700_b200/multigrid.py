@@ -147,6 +147,10 @@ class _DeviceVCycle:
     def _block_lams(self):
         raise NotImplementedError
 
+    def _halo(self, level, t):
+        """refresh the halo planes of t before an operator application / transfer reads them
+        (no-op on a whole-mesh hierarchy; slab.DistMultiBlockSolver exchanges them)"""
+
     # ---- device kernels per level ----
     def _thetas(self, level):
         return [sm.theta for sm in self._level_smoothers(level)]
@@ -175,6 +179,7 @@ class _DeviceVCycle:
                 _lib.call("spk_cheb_init", h.ctx, level, nb, lams, self.tau, thetas, ptr(b), ptr(lv.r), ptr(lv.x),
                           ptr(lv.d), st)
             else:
+                self._halo(level, lv.x)
                 _lib.call("spk_residual", h.ctx, level, nb, lams, self.tau, ptr(lv.x), ptr(b), ptr(lv.r),
                           ptr(lv.d), thetas, st)
         deg = self.config.smoother_degree
@@ -185,6 +190,7 @@ class _DeviceVCycle:
         coefs = [sm.coefficients() for sm in sms]
         for k in range(deg - 1):
             final = 1 if k == deg - 2 else 0  # last step also performs "return x + d" (fused)
+            self._halo(level, lv.d)
             if self.pair:
                 c1, c2 = coefs[0][k]
                 _lib.call("spk_pair_cheb_step", h.ctx, level, self.re_lam, self.im_lam, self.tau, c1, c2,
@@ -203,8 +209,10 @@ class _DeviceVCycle:
             _lib.call("spk_pair_residual", h.ctx, level, self.re_lam, self.im_lam, self.tau, ptr(lv.x), ptr(b),
                       ptr(lv.r), None, 1.0, st)
         else:
+            self._halo(level, lv.x)
             _lib.call("spk_residual", h.ctx, level, self.nrows, _lib.dbl_array(self._block_lams()), self.tau,
                       ptr(lv.x), ptr(b), ptr(lv.r), None, None, st)
+        self._halo(level, lv.r)
         h.restrict_into(level, lv.r, self._bufs[level - 1].b, mask=True)
 
     def _ensure(self):

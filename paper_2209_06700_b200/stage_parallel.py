@@ -1,14 +1,15 @@
 """Stage-parallel Radau IIA step across GPUs (the paper's layout).
 
-Rank r of the stage communicator owns a contiguous group of stages (Q / world each; the mesh is not
-partitioned, B = 1), so every block solve of eq. irk:P runs locally with no inter-stage traffic.
-Only three kinds of exchange remain:
+Rank (s, b) of a `runtime.RankGrid` owns stage group s (a contiguous range of the Q stages) of mesh
+partition b (B = 1: the whole mesh; B > 1: an x-slab, `slab.SlabPartition`), so every block solve
+of eq. irk:P runs inside its column group with no inter-stage traffic. The exchanges are:
 
 * stage combines (D (x) I) u for D in {S~^-1, S~, A^-1}: a Cannon-like ring (`RingCombiner`): in round
   s rank r holds the stage group of rank (r + s) mod world, adds D[own, held] @ held, and passes it on
   (world - 1 shifts of one stage group; grouped isend/irecv, NCCL over NVLink on the GPU path);
 * GMRES inner products: local partial dot + all-reduce (fixed order, deterministic per run);
-* nothing else: the right-hand side and the update are stage-local.
+* halo planes on the column group before each operator application (B > 1 only);
+* the update u + tau sum_i b_i k_i: partial sums all-reduced on the row group.
 
 The driver is backend-agnostic: `backend` supplies the stage-local operators. `GPUStageBackend` uses
 the device kernels (K1 block mode, MultiBlockSolver, spk_rhs); tests/test_stage_parallel_gloo.py runs the
@@ -20,25 +21,20 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .runtime import Counters, RankGrid, all_reduce_sum, host_staged, stage_groups  # noqa: F401
 from .tableau import crout_lu, radau_iia, spectral_real
 
 
-def stage_groups(Q, world):
-    """Contiguous stage ranges per rank (as equal as possible)."""
-    base, extra = divmod(Q, world)
-    out, s = [], 0
-    for r in range(world):
-        c = base + (1 if r < extra else 0)
-        out.append((s, s + c))
-        s += c
-    return out
-
-
 class RingCombiner:
-    """v_own = sum_j D[own, j] x_j with x distributed by stage groups (Cannon-like rotation)."""
+    """v_own = sum_j D[own, j] x_j with x distributed by stage groups (Cannon-like rotation).
 
-    def __init__(self, groups, rank, world, group=None):
+    `rank` is the position in the ring (the stage group index), `world` the ring length; `ranks`
+    maps ring positions to global ranks (default: identity, the default group)."""
+
+    def __init__(self, groups, rank, world, group=None, ranks=None, counters=None):
         self.groups, self.rank, self.world, self.group = groups, rank, world, group
+        self.ranks = list(ranks) if ranks is not None else list(range(world))
+        self.counters = counters if counters is not None else Counters()
         self.shift_rounds = 0
 
     def __call__(self, D, x_local, in_groups=None, out_groups=None):
@@ -62,29 +58,36 @@ class RingCombiner:
             if s < W - 1:
                 send = torch.zeros((maxg, n), dtype=x_local.dtype, device=x_local.device)
                 send[: held.shape[0]] = held[: hhi - hlo]
-                recv = torch.empty_like(send)
-                ops = [dist.P2POp(dist.isend, send, self.groups_rank((r - 1) % W), self.group),
+                wire = host_staged(send, self.group)
+                recv = torch.empty_like(wire)
+                ops = [dist.P2POp(dist.isend, wire, self.groups_rank((r - 1) % W), self.group),
                        dist.P2POp(dist.irecv, recv, self.groups_rank((r + 1) % W), self.group)]
                 for req in dist.batch_isend_irecv(ops):
                     req.wait()
-                held = recv
+                held = recv.to(x_local.device)
                 held_owner = (held_owner + 1) % W
                 self.shift_rounds += 1
+                self.counters.shift_rounds += 1
+                self.counters.add_send(wire)
         return out
 
     def groups_rank(self, r):
-        return r  # ranks of the stage communicator are 0..world-1 in the default group
+        return self.ranks[r]
 
 
 class DistKrylov:
-    """Right-preconditioned MGS GMRES (krylov.py:28-103 semantics) with all-reduced inner products."""
+    """Right-preconditioned MGS GMRES (krylov.py:28-103 semantics) with all-reduced inner products.
 
-    def __init__(self, group=None):
+    `owned(v)` selects the entries a rank owns (slab halos excluded from the dots)."""
+
+    def __init__(self, group=None, owned=None, counters=None):
         self.group = group
+        self.owned = owned or (lambda v: v)
+        self.counters = counters
 
     def dot(self, a, b):
-        t = torch.sum(a * b).reshape(1).to(torch.float64)
-        dist.all_reduce(t, group=self.group)
+        t = torch.sum(self.owned(a) * self.owned(b)).reshape(1).to(torch.float64)
+        all_reduce_sum(t, self.group, self.counters)
         return float(t.item())
 
     def solve(self, A, P, b, rel_tol=1e-12, max_iter=200):
@@ -130,7 +133,8 @@ class DistKrylov:
 class StageParallelStepper:
     """eq. irk:A solved by GMRES with the eq. irk:P preconditioner, stages distributed over ranks."""
 
-    def __init__(self, backend, Q, tau, rank, world, group=None, tableau=None, rel_tol=1e-12, max_iter=200):
+    def __init__(self, backend, Q, tau, rank, world, group=None, tableau=None, rel_tol=1e-12, max_iter=200,
+                 grid=None):
         self.be, self.Q, self.tau = backend, Q, float(tau)
         self.rank, self.world = rank, world
         self.rel_tol, self.max_iter = rel_tol, max_iter
@@ -139,10 +143,22 @@ class StageParallelStepper:
         self.A, self.b, self.c, self.Ainv = get(tab, "A"), get(tab, "b"), get(tab, "c"), get(tab, "Ainv")
         sp = spectral_real(crout_lu(self.Ainv).L)
         self.lams, self.S, self.Sinv = sp.lambdas, sp.S, sp.Sinv
-        self.groups = stage_groups(Q, world)
-        self.lo, self.hi = self.groups[rank]
-        self.ring = RingCombiner(self.groups, rank, world, group)
-        self.kry = DistKrylov(group)
+        # rank grid: default = every rank its own stage group, one mesh partition (B = 1)
+        self.grid = grid if grid is not None else RankGrid(world, 1)
+        if self.grid.size != world and self.grid.topology != "row_major_padded":
+            raise ValueError(f"rank grid spans {self.grid.size} ranks, world has {world}")
+        sb = self.grid.coords(rank)
+        if sb is None:
+            raise ValueError(f"rank {rank} is idle in the {self.grid.topology} grid")
+        self.s_idx, self.b_idx = sb
+        S = self.grid.S
+        self.groups = stage_groups(Q, S)
+        self.lo, self.hi = self.groups[self.s_idx]
+        row_group = self.grid.row_group(self.b_idx) if self.grid.B > 1 else group
+        self.row_group = row_group
+        self.ring = RingCombiner(self.groups, self.s_idx, S, row_group, ranks=self.grid.row_ranks(self.b_idx),
+                                 counters=self.grid.counters)
+        self.kry = DistKrylov(group, owned=getattr(backend, "owned", None), counters=self.grid.counters)
         backend.setup(self.lams[self.lo : self.hi], self.tau)
 
     def A_op(self, k):
@@ -163,7 +179,8 @@ class StageParallelStepper:
         # u_{n+1} = u_n + tau sum_i b_i k_i: partial sum over own stages, all-reduced
         part = self.tau * torch.einsum("i,in->n", torch.as_tensor(self.b[self.lo : self.hi], dtype=k.dtype,
                                                                   device=k.device), k)
-        dist.all_reduce(part, group=self.kry.group)
+        if self.grid.S > 1:
+            all_reduce_sum(part, self.row_group, self.grid.counters)
         return u_n + part, its, conv
 
 
@@ -202,6 +219,43 @@ class GPUStageBackend:
 
     def stage_rhs(self, t_n, u_n, ctau):
         um = torch.where(self.maskt, u_n, torch.zeros_like(u_n)).reshape(1, -1)
+        ku = self.h.apply_block(self.L, 0.0, 1.0, um)[0]
+        fhat = torch.empty_like(u_n)
+        from . import _lib
+        from ._device import ptr, stream_ptr
+        _lib.call("spk_outer3", self.h.ctx, self.L, ptr(self.g1), ptr(fhat), stream_ptr(self.h.device))
+        return torch.stack([self.source.F(t_n + ct) * fhat - ku for ct in ctau])
+
+
+class GPUSlabStageBackend(GPUStageBackend):
+    """Stage-local device operators on an x-slab of the mesh (B > 1): halo exchange on the column
+    group before each operator application, distributed V-cycles (slab.DistMultiBlockSolver), dots
+    over the owned planes only."""
+
+    def __init__(self, slab_hierarchy, config=None, source=None):
+        super().__init__(slab_hierarchy, config, source)
+        self.part = slab_hierarchy.part
+        self.win = slab_hierarchy.window(self.L)
+
+    def setup(self, lams, tau):
+        from .slab import DistMultiBlockSolver
+
+        self.tau = tau
+        self.solver = DistMultiBlockSolver(self.h, lams, tau, self.config) if len(lams) else None
+        self.g1 = torch.from_numpy(self.h.load_vector_1d(self.L, self.source.s)).to(self.h.device)
+        self.maskt = self.h.mask_tensor(self.L)
+
+    def owned(self, v):
+        return self.win.owned(v)
+
+    def mass_stiff(self, k):
+        km = torch.where(self.maskt, k, torch.zeros_like(k))
+        self.part.exchange(km, self.L)
+        return (self.h.apply_block(self.L, 1.0, 0.0, km), self.h.apply_block(self.L, 0.0, 1.0, km))
+
+    def stage_rhs(self, t_n, u_n, ctau):
+        um = torch.where(self.maskt, u_n, torch.zeros_like(u_n)).reshape(1, -1)
+        self.part.exchange(um, self.L)
         ku = self.h.apply_block(self.L, 0.0, 1.0, um)[0]
         fhat = torch.empty_like(u_n)
         from . import _lib
