@@ -126,7 +126,7 @@ def _vcycle_worker(rank, world, k, L, deg):
     ref = MultiBlockSolver(full, lams, 1e-2, cfg)
     dsv = DistMultiBlockSolver(sh, lams, 1e-2, cfg)
     lam_err = max(abs(np.asarray(dsv.lambda_max[l]) - np.asarray(ref.lambda_max[l])).max() /
-                  np.abs(ref.lambda_max[l]).max() for l in range(L + 1))
+                  np.abs(ref.lambda_max[l]).max() for l in range(part.gather_level, L + 1))
     b = torch.rand((2, full.n), generator=torch.Generator().manual_seed(3), dtype=torch.float64).cuda()
     x_ref = ref.apply_device(b)
     x = dsv.apply_device(part.scatter(b, L))
