@@ -23,6 +23,8 @@
  *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
  *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
  *   spk_mask                GridHierarchy.constrain                       fem.py:153-158
+ *   spk_peer_combine        SPEC tensor_ops sharedmem_combine (D (x) I) u
+ *   spk_ipc_*               peer windows of the shared-memory backend     SPEC.md:354 (runtime DESIGN)
  *   spk_ctx_set_slab        (no reference code: the paper's spatial partition inside a stage
  *                           group; SPEC RankGrid partitions b)
  */
@@ -113,6 +115,17 @@ int spk_combine(spk_ctx* ctx, int mask_level, long long n, int nin, int nout, co
                 void* stream);
 
 /* GMRES: w -= (*h_prev) v_prev ; *out = <v_cur, w>  (v_cur == NULL: *out = ||w||) */
+/* out_o = sum_j D[o, j] in_rows[j] over n entries; in_rows is a HOST array of nin device pointers,
+ * which may point into peer GPUs' memory (CUDA IPC windows): the stage exchange and the combine
+ * arithmetic are one kernel reading over NVLink (the shared-memory combine backend) */
+int spk_peer_combine(long long n, int nin, const double* const* in_rows, int nout, const double* D,
+                     double* out, long long sout, int accumulate, void* stream);
+/* peer windows: cudaMalloc'd buffer + its 64-byte IPC handle; open / close a peer's window */
+int spk_ipc_alloc(long long bytes, void** dev_ptr, void* handle64);
+int spk_ipc_open(const void* handle64, void** dev_ptr);
+int spk_ipc_close(void* dev_ptr);
+int spk_ipc_free(void* dev_ptr);
+int spk_copy_d2d(void* dst, const void* src, long long bytes, void* stream);
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
             const double* v_cur, double* out, void* stream);
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);

@@ -57,6 +57,12 @@ _SIGS = {
     "spk_transfer": ([c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_vp], c_int),
     "spk_axpy_flag": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_combine": ([c_vp, c_int, c_ll, c_int, c_int, P_dbl, c_vp, c_ll, c_vp, c_ll, c_int, c_vp], c_int),
+    "spk_peer_combine": ([c_ll, c_int, c_vp, c_int, P_dbl, c_vp, c_ll, c_int, c_vp], c_int),
+    "spk_ipc_alloc": ([c_ll, ctypes.POINTER(c_vp), c_vp], c_int),
+    "spk_ipc_open": ([c_vp, ctypes.POINTER(c_vp)], c_int),
+    "spk_ipc_close": ([c_vp], c_int),
+    "spk_ipc_free": ([c_vp], c_int),
+    "spk_copy_d2d": ([c_vp, c_vp, c_ll, c_vp], c_int),
     "spk_mgs": ([c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_scale_div": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_lincomb": ([c_ll, c_int, c_vp, c_vp, c_vp, c_vp], c_int),

@@ -637,7 +637,8 @@ int spk_combine(spk_ctx* c, int mask_level, long long n, int nin, int nout, cons
     return fail(SPK_EUNSUPPORTED, "combine supports up to 18 rows/columns");
   SpkCombineArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.in = in; a.out = out; a.n = n; a.sin = sin; a.sout = sout;
+  for (int j = 0; j < nin; ++j) a.in[j] = in + j * sin;
+  a.out = out; a.n = n; a.sin = sin; a.sout = sout;
   a.nin = nin; a.nout = nout; a.accumulate = accumulate;
   if (mask_level >= 0) {
     if (int rc = check_level(c, mask_level)) return rc;
@@ -648,6 +649,61 @@ int spk_combine(spk_ctx* c, int mask_level, long long n, int nin, int nout, cons
     for (int j = 0; j < nin; ++j) a.D[o * SPK_CMAX + j] = D[o * nin + j];
   cudaError_t e = spk_launch_combine(a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "combine");
+  return SPK_OK;
+}
+
+int spk_peer_combine(long long n, int nin, const double* const* in_rows, int nout, const double* D,
+                     double* out, long long sout, int accumulate, void* stream) {
+  if (nin < 1 || nout < 1 || nin > SPK_CMAX || nout > SPK_CMAX)
+    return fail(SPK_EUNSUPPORTED, "peer combine supports up to 18 rows/columns");
+  SpkCombineArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int j = 0; j < nin; ++j) a.in[j] = in_rows[j];
+  a.out = out; a.n = n; a.sout = sout;
+  a.nin = nin; a.nout = nout; a.accumulate = accumulate;
+  for (int o = 0; o < nout; ++o)
+    for (int j = 0; j < nin; ++j) a.D[o * SPK_CMAX + j] = D[o * nin + j];
+  cudaError_t e = spk_launch_combine(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "peer combine");
+  return SPK_OK;
+}
+
+int spk_ipc_alloc(long long bytes, void** dev_ptr, void* handle) {
+  if (!dev_ptr || !handle || bytes <= 0) return fail(SPK_ECONFIG, "bad ipc allocation request");
+  cudaError_t e = cudaMalloc(dev_ptr, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ipc window)");
+  e = cudaMemset(*dev_ptr, 0, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(ipc window)");
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, sizeof(h));
+  return SPK_OK;
+}
+
+int spk_ipc_open(const void* handle, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return SPK_OK;
+}
+
+int spk_ipc_close(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return SPK_OK;
+}
+
+int spk_ipc_free(void* dev_ptr) {
+  cudaError_t e = cudaFree(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFree(ipc window)");
+  return SPK_OK;
+}
+
+int spk_copy_d2d(void* dst, const void* src, long long bytes, void* stream) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
   return SPK_OK;
 }
 

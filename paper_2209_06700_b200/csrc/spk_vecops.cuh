@@ -34,7 +34,7 @@ struct SpkTransferArgs {
 };
 
 struct SpkCombineArgs {
-  const double* in;
+  const double* in[SPK_CMAX];  // input rows (local rows, or rows in peer GPUs' memory)
   double* out;
   long long n, sin, sout;
   int nin, nout, mask, accumulate;

@@ -164,7 +164,7 @@ __global__ void combine_kernel(const __grid_constant__ SpkCombineArgs a) {
     double in[SPK_CMAX];
 #pragma unroll
     for (int j = 0; j < SPK_CMAX; ++j)
-      if (j < a.nin) in[j] = a.in[j * a.sin + i];
+      if (j < a.nin) in[j] = a.in[j][i];
     for (int o = 0; o < a.nout; ++o) {
       double s = 0.0;
 #pragma unroll

@@ -75,6 +75,121 @@ class RingCombiner:
         return self.ranks[r]
 
 
+class CudaIpcWindows:
+    """Peer windows in device memory: cudaMalloc'd buffers exported / imported with CUDA IPC
+    (`spk_ipc_*`); peers map them over NVLink (lazy peer access)."""
+
+    def __init__(self, device):
+        self.device = device
+
+    def create(self, nbytes):
+        from . import _lib
+        p = _lib.c_vp()
+        h = (_lib.ctypes.c_char * 64)()
+        _lib.call("spk_ipc_alloc", int(nbytes), _lib.ctypes.byref(p), h)
+        return p.value, bytes(h)
+
+    def open(self, handle):
+        from . import _lib
+        p = _lib.c_vp()
+        buf = (_lib.ctypes.c_char * 64).from_buffer_copy(handle)
+        _lib.call("spk_ipc_open", buf, _lib.ctypes.byref(p))
+        return p.value
+
+    def row(self, ptr, i, n):
+        return ptr + i * n * 8
+
+    def write(self, ptr, x):
+        from . import _lib
+        from ._device import stream_ptr
+        x = x.contiguous()
+        _lib.call("spk_copy_d2d", ptr, x.data_ptr(), x.numel() * 8, stream_ptr(self.device))
+
+    def combine(self, n, rows, D, out):
+        from . import _lib
+        from ._device import stream_ptr
+        D = np.ascontiguousarray(D, dtype=float)
+        table = (_lib.c_vp * len(rows))(*rows)
+        _lib.call("spk_peer_combine", n, len(rows), table, D.shape[0], D.ctypes.data_as(_lib.P_dbl),
+                  out.data_ptr(), out.stride(0), 0, stream_ptr(self.device))
+
+    def sync(self):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def close(self, peer_ptrs, own):
+        from . import _lib
+        for p in peer_ptrs:
+            _lib.call("spk_ipc_close", p)
+        _lib.call("spk_ipc_free", own)
+
+
+class PeerCombiner:
+    """Shared-memory stage combine (SPEC tensor_ops sharedmem_combine; the paper's
+    shared-memory virtual topology): every rank of the row group exposes its
+    stage group in a peer window; between two row barriers each rank reads the peers' rows directly
+    and combines them in ONE kernel (`spk_peer_combine`: the loads over NVLink are the exchange).
+    No messages, 2 barriers per call. Same interface as RingCombiner."""
+
+    def __init__(self, groups, rank, world, group=None, ranks=None, counters=None, windows=None, device=None):
+        self.groups, self.rank, self.world, self.group = groups, rank, world, group
+        self.ranks = list(ranks) if ranks is not None else list(range(world))
+        self.counters = counters if counters is not None else Counters()
+        self.windows = windows if windows is not None else CudaIpcWindows(device)
+        self.shift_rounds = 0
+        self._own = None
+        self._n = None
+
+    def _setup(self, n, rows_max):
+        own, handle = self.windows.create(rows_max * n * 8)
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, handle, group=self.group)
+        else:
+            handles = [handle]
+        self._own = own
+        self._peers = [own if r == self.rank else self.windows.open(h) for r, h in enumerate(handles)]
+        self._n, self._rows_max = n, rows_max
+
+    def _barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        self.counters.barrier_count += 1
+
+    def __call__(self, D, x_local, in_groups=None, out_groups=None):
+        D = np.asarray(D)
+        ig = in_groups or self.groups
+        og = out_groups or self.groups
+        lo, hi = og[self.rank]
+        n = x_local.shape[-1]
+        rows_max = max(max(g[1] - g[0] for g in ig), 1)
+        if self._own is None or self._n != n or self._rows_max < rows_max:
+            if self._own is not None:
+                self.close()
+            self._setup(n, rows_max)
+        ilo, ihi = ig[self.rank]
+        if ihi > ilo:
+            self.windows.write(self._own, x_local[: ihi - ilo])
+        self.windows.sync()
+        self._barrier()  # every window holds its rank's current rows
+        out = torch.zeros((hi - lo, n), dtype=x_local.dtype, device=x_local.device)
+        rows = []
+        for r, (a, b) in enumerate(ig):
+            rows.extend(self.windows.row(self._peers[r], i, n) for i in range(b - a))
+        if hi > lo and rows:
+            self.windows.combine(n, rows, D[lo:hi, : len(rows)], out)
+        self.windows.sync()
+        self._barrier()  # nobody overwrites a window before every rank has read it
+        return out
+
+    def close(self):
+        """Collective: release the peer mappings and the own window."""
+        if self._own is None:
+            return
+        self._barrier()
+        self.windows.close([p for r, p in enumerate(self._peers) if r != self.rank], self._own)
+        self._own = None
+
+
 class DistKrylov:
     """Right-preconditioned MGS GMRES (krylov.py:28-103 semantics) with all-reduced inner products.
 
@@ -134,7 +249,7 @@ class StageParallelStepper:
     """eq. irk:A solved by GMRES with the eq. irk:P preconditioner, stages distributed over ranks."""
 
     def __init__(self, backend, Q, tau, rank, world, group=None, tableau=None, rel_tol=1e-12, max_iter=200,
-                 grid=None):
+                 grid=None, combine="ring", windows=None):
         self.be, self.Q, self.tau = backend, Q, float(tau)
         self.rank, self.world = rank, world
         self.rel_tol, self.max_iter = rel_tol, max_iter
@@ -156,8 +271,15 @@ class StageParallelStepper:
         self.lo, self.hi = self.groups[self.s_idx]
         row_group = self.grid.row_group(self.b_idx) if self.grid.B > 1 else group
         self.row_group = row_group
-        self.ring = RingCombiner(self.groups, self.s_idx, S, row_group, ranks=self.grid.row_ranks(self.b_idx),
-                                 counters=self.grid.counters)
+        if combine == "ring":
+            self.ring = RingCombiner(self.groups, self.s_idx, S, row_group, ranks=self.grid.row_ranks(self.b_idx),
+                                     counters=self.grid.counters)
+        elif combine == "peer":
+            self.ring = PeerCombiner(self.groups, self.s_idx, S, row_group, ranks=self.grid.row_ranks(self.b_idx),
+                                     counters=self.grid.counters, windows=windows,
+                                     device=getattr(getattr(backend, "h", None), "device", None))
+        else:
+            raise ValueError(f"unknown combine backend {combine!r}")
         self.kry = DistKrylov(group, owned=getattr(backend, "owned", None), counters=self.grid.counters)
         backend.setup(self.lams[self.lo : self.hi], self.tau)
 

@@ -144,7 +144,7 @@ def test_distributed_vcycle_matches_whole_mesh(cuda, k, L, world, deg):
 
 
 # ---------------------------------------------------------------------------------------------
-def _stepper_worker(rank, world, S, B, topology):
+def _stepper_worker(rank, world, S, B, topology, combine="ring"):
     from oracle.tableau_ref import radau_iia
     from paper_2209_06700_b200.fem import build_hierarchy
     from paper_2209_06700_b200.irk import StageSystem
@@ -161,7 +161,8 @@ def _stepper_worker(rank, world, S, B, topology):
     sh = SlabHierarchy(L, k, part, device="cuda:0")
     cfg = VCycleConfig(smoother_degree=3)
     tab = radau_iia(Q)
-    sp = StageParallelStepper(GPUSlabStageBackend(sh, cfg), Q, tau, rank, world, tableau=tab, grid=grid)
+    sp = StageParallelStepper(GPUSlabStageBackend(sh, cfg), Q, tau, rank, world, tableau=tab, grid=grid,
+                              combine=combine)
     ss = StageSystem(build_hierarchy(3, L, k, device="cuda:0"), Q, tau, config=cfg, tableau=tab)
     u_ref = ss.initial_condition()
     u = part.scatter(u_ref.reshape(1, -1), L)[0]
@@ -171,16 +172,72 @@ def _stepper_worker(rank, world, S, B, topology):
         u, k_it, conv = sp.step(st * tau, u)
         its.append((k_it, rep.iterations, conv))
     ug = part.gather(u.reshape(1, -1), L)[0]
+    if combine == "peer":
+        sp.ring.close()
     return (float((ug - u_ref).abs().max() / u_ref.abs().max()), its, grid.snapshot(rank))
 
 
-@pytest.mark.parametrize("S,B,topology", [(1, 2, "row_major"), (3, 2, "row_major"), (2, 2, "column_major")])
-def test_stage_parallel_slab_stepper(cuda, S, B, topology):
-    res = _run(_stepper_worker, S * B, S, B, topology)
+@pytest.mark.parametrize("S,B,topology,combine", [(1, 2, "row_major", "ring"), (3, 2, "row_major", "ring"),
+                                                  (2, 2, "column_major", "ring"), (3, 1, "row_major", "peer"),
+                                                  (2, 2, "row_major", "peer")])
+def test_stage_parallel_slab_stepper(cuda, S, B, topology, combine):
+    if B == 1:
+        pytest.skip("B = 1 runs through the whole-mesh backend below")
+    res = _run(_stepper_worker, S * B, S, B, topology, combine)
     for r, (err, its, snap) in res.items():
         assert err < 1e-9, (r, err)
         for k_it, k_ref, conv in its:
             assert conv and abs(k_it - k_ref) <= 1, its
         assert snap["halo_exchanges"] > 0
-        if S > 1:
+        if S > 1 and combine == "ring":
             assert snap["shift_rounds"] > 0 and snap["shift_rounds"] % (S - 1) == 0
+        if combine == "peer":
+            assert snap["shift_rounds"] == 0 and snap["barriers"] > 0
+
+
+def _peer_worker(rank, world, Q):
+    """B = 1, one stage group per rank: peer-window combines (CUDA IPC) vs the ring vs one GPU."""
+    from oracle.tableau_ref import radau_iia
+    from paper_2209_06700_b200.fem import build_hierarchy
+    from paper_2209_06700_b200.irk import StageSystem
+    from paper_2209_06700_b200.multigrid import VCycleConfig
+    from paper_2209_06700_b200.stage_parallel import (GPUStageBackend, PeerCombiner, RingCombiner,
+                                                      StageParallelStepper, stage_groups)
+
+    h = build_hierarchy(3, 3, 2, device="cuda:0")
+    cfg = VCycleConfig(smoother_degree=3)
+    tab = radau_iia(Q)
+    # raw combines: random D, x
+    groups = stage_groups(Q, world)
+    lo, hi = groups[rank]
+    g = torch.Generator().manual_seed(11)
+    D = torch.rand((Q, Q), generator=g, dtype=torch.float64).numpy()
+    X = torch.rand((Q, 5000), generator=g, dtype=torch.float64).cuda()
+    pc = PeerCombiner(groups, rank, world, device=torch.device("cuda", 0))
+    rc = RingCombiner(groups, rank, world)
+    vp = pc(D, X[lo:hi])
+    vr = rc(D, X[lo:hi])
+    vd = torch.from_numpy(D[lo:hi]).cuda() @ X
+    comb_err = max(float((vp - vd).abs().max() / vd.abs().max()), float((vr - vd).abs().max() / vd.abs().max()))
+    sp = StageParallelStepper(GPUStageBackend(h, cfg), Q, 0.01, rank, world, tableau=tab, combine="peer")
+    ss = StageSystem(h, Q, 0.01, config=cfg, tableau=tab)
+    u1 = ss.initial_condition()
+    u2 = u1.clone()
+    its = []
+    for st in range(2):
+        u1, rep = ss.step(st * 0.01, u1)
+        u2, k_it, conv = sp.step(st * 0.01, u2)
+        its.append((k_it, rep.iterations, conv))
+    sp.ring.close()
+    pc.close()
+    return comb_err, float((u2 - u1).abs().max() / u1.abs().max()), its
+
+
+@pytest.mark.parametrize("Q,world", [(3, 3), (4, 2)])
+def test_peer_window_combine_stepper(cuda, Q, world):
+    res = _run(_peer_worker, world, Q)
+    for r, (comb_err, err, its) in res.items():
+        assert comb_err < 1e-14, (r, comb_err)
+        assert err < 1e-9, (r, err)
+        for k_it, k_ref, conv in its:
+            assert conv and abs(k_it - k_ref) <= 1

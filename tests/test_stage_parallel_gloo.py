@@ -48,7 +48,51 @@ class OracleStageBackend:
         return torch.from_numpy(np.stack([self.h.load_vector(self.L, self.src.f, t_n + ct) - ku for ct in ctau]))
 
 
-def _worker(rank, world, port, Q, q_out):
+class HostShmWindows:
+    """Test double of CudaIpcWindows: POSIX shared memory between the gloo processes."""
+
+    def __init__(self):
+        self._shm = {}
+
+    def _arr(self, name):
+        shm = self._shm[name]
+        return np.ndarray((shm.size // 8,), dtype=np.float64, buffer=shm.buf)
+
+    def create(self, nbytes):
+        from multiprocessing import shared_memory
+        shm = shared_memory.SharedMemory(create=True, size=nbytes)
+        self._shm[shm.name] = shm
+        return shm.name, shm.name.encode()
+
+    def open(self, handle):
+        from multiprocessing import shared_memory
+        name = handle.decode()
+        self._shm[name] = shared_memory.SharedMemory(name=name)
+        return name
+
+    def row(self, ptr, i, n):
+        return (ptr, i * n, n)
+
+    def write(self, ptr, x):
+        x = x.reshape(-1).numpy()
+        self._arr(ptr)[: x.size] = x
+
+    def combine(self, n, rows, D, out):
+        X = np.stack([self._arr(p)[o : o + m] for p, o, m in rows])
+        out.copy_(torch.from_numpy(np.asarray(D) @ X))
+
+    def sync(self):
+        pass
+
+    def close(self, peer_ptrs, own):
+        for p in peer_ptrs:
+            self._shm.pop(p).close()
+        shm = self._shm.pop(own)
+        shm.close()
+        shm.unlink()
+
+
+def _worker(rank, world, port, Q, q_out, combine="ring"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,22 +102,26 @@ def _worker(rank, world, port, Q, q_out):
 
         be = OracleStageBackend(3, 3, 1, 5)
         tab = radau_iia(Q)
-        sp = StageParallelStepper(be, Q, 0.05, rank, world, tableau=tab)
+        sp = StageParallelStepper(be, Q, 0.05, rank, world, tableau=tab, combine=combine,
+                                  windows=HostShmWindows() if combine == "peer" else None)
         u = torch.from_numpy(be.src.u(be.h.node_coords(be.L), 0.0))
         its = []
         for s in range(2):
             u, k, conv = sp.step(s * 0.05, u)
             its.append(k)
+        if combine == "peer":
+            sp.ring.close()
         if rank == 0:
-            q_out.put((u.numpy(), its, sp.ring.shift_rounds))
+            q_out.put((u.numpy(), its, sp.ring.shift_rounds, sp.grid.counters.as_dict()))
     except Exception as e:  # pragma: no cover
         q_out.put(repr(e))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("Q,world", [(2, 2), (3, 2), (4, 2)])
-def test_stage_parallel_matches_oracle(Q, world):
+@pytest.mark.parametrize("Q,world,combine", [(2, 2, "ring"), (3, 2, "ring"), (4, 2, "ring"), (4, 4, "peer"),
+                                              (3, 2, "peer")])
+def test_stage_parallel_matches_oracle(Q, world, combine):
     from oracle import stepper
     from oracle.fem_qk import Hierarchy
     from oracle.tableau_ref import radau_iia
@@ -84,14 +132,14 @@ def test_stage_parallel_matches_oracle(Q, world):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, Q, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, Q, q, combine)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(300)
     res = q.get()
     assert not isinstance(res, str), res
-    u_dist, its_dist, shifts = res
+    u_dist, its_dist, shifts, counters = res
     ref = stepper.RealLU(Hierarchy(3, 3, 1), Q, 0.05, tab=radau_iia(Q))
     u = ref.initial()
     its = []
@@ -100,9 +148,14 @@ def test_stage_parallel_matches_oracle(Q, world):
         its.append(k)
     assert all(abs(a - b) <= 1 for a, b in zip(its_dist, its)), (its_dist, its)
     assert np.abs(u_dist - u).max() / np.abs(u).max() < 1e-9
-    # (world - 1) ring shifts per combine, 3 combines per GMRES iteration (+ 1 for the RHS, the final
-    # P^-1 and A) -> strictly positive and a multiple of world - 1
-    assert shifts > 0 and shifts % (world - 1) == 0
+    if combine == "ring":
+        # (world - 1) ring shifts per combine, 3 combines per GMRES iteration (+ 1 for the RHS, the
+        # final P^-1 and A) -> strictly positive and a multiple of world - 1
+        assert shifts > 0 and shifts % (world - 1) == 0
+    else:
+        # shared-memory backend: no messages for the combines, 2 barriers per combine
+        assert shifts == 0 and counters["shift_rounds"] == 0
+        assert counters["barriers"] > 0 and counters["barriers"] % 2 == 1  # + 1 for close()
 
 
 class OracleComplexBackend(OracleStageBackend):
