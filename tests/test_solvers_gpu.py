@@ -248,3 +248,19 @@ def test_direct_complex_parallel_gpu_backend_single_rank(cuda):
         assert rel(u2.cpu().numpy(), u1.cpu().numpy()) < 1e-9
     finally:
         dist.destroy_process_group()
+
+
+def test_perfmodel_counters_on_device_steps(cuda):
+    """#V = Q (#G + 1) per step in the real-LU path; predicted stage-parallel speedup = Q."""
+    from paper_2209_06700_b200.perfmodel import validate_against_counters
+
+    h = build_hierarchy(3, 3, 2)
+    ss = StageSystem(h, 4, 0.01, config=VCycleConfig(smoother_degree=3), tableau=ref_radau(4))
+    u = ss.initial_condition()
+    reps = []
+    for s in range(2):
+        u, rep = ss.step(s * 0.01, u)
+        reps.append(rep)
+    v = validate_against_counters(reps, 4)
+    assert v.ok, v.mismatches
+    assert v.predicted_speedup == 4
