@@ -420,54 +420,36 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, (EPI == EPI_STORE || Q <= 2) ? 
 
   // ---- fixed per-thread work descriptors ----
   const long long plane_stride = (long long)g.ny * g.nz;
-  // U-plane load items: slots outside the domain are zeroed once (in both buffers) and never
-  // loaded; in-domain slots get one 8-byte cp.async per plane (zero-fill only for constrained
-  // boundary nodes).
-  const double* lsrc[G::LIT];
-  unsigned ldst[G::LIT];
-  bool lbnd[G::LIT];
+  // U-plane load items, fixed for the kernel: a 32-bit source offset (doubles from u), the shared
+  // address and a byte count (8, or 0 = zero-fill: slots outside the domain and, constrained,
+  // y/z-boundary nodes). One zero-filling 8-byte cp.async per item and plane, no branches.
+  unsigned loff[G::LIT], ldst[G::LIT], lnb[G::LIT];
+  constexpr bool LTAIL = (G::LITEMS % NT) != 0;  // only the last item can be past the end
 #pragma unroll
   for (int i = 0; i < G::LIT; ++i) {
-    const int idx = tid + i * NT;
-    lsrc[i] = nullptr;
-    ldst[i] = 0u;
-    lbnd[i] = false;
-    if (idx < G::LITEMS) {
-      const int q = idx / (NYin * NZin);
-      const int rem = idx - q * (NYin * NZin);
-      const int yy = rem / NZin, zz = rem - yy * NZin;
-      const int gy = y_lo - K + yy, gz = z_lo - K + zz;
-      const int slot = (q * NYin + yy) * NZp + zz;
-      if (gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz) {
-        ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
-        lsrc[i] = u + (long long)q * a.su + (long long)gy * g.nz + gz;
-        lbnd[i] = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
-      } else {
-        Us[slot] = 0.0;
-        Us[G::U_SZ + slot] = 0.0;
-      }
-    }
+    const int idx = min(tid + i * NT, G::LITEMS - 1);
+    const int q = idx / (NYin * NZin);
+    const int rem = idx - q * (NYin * NZin);
+    const int yy = rem / NZin, zz = rem - yy * NZin;
+    const int gy = y_lo - K + yy, gz = z_lo - K + zz;
+    const int slot = (q * NYin + yy) * NZp + zz;
+    ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
+    const bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
+    const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
+    loff[i] = in ? static_cast<unsigned>(q * a.su + (long long)gy * g.nz + gz) : 0u;
+    lnb[i] = (in && !(a.constrained && bnd)) ? 8u : 0u;
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
   auto load_plane = [&](int x, int buf) {
-    const long long xoff = (long long)x * plane_stride;
-    if (!a.constrained) {
+    const double* base = u + (long long)x * plane_stride;
+    // constrained: the x-boundary planes are zero (uniform per plane)
+    const bool xb = a.constrained && !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
 #pragma unroll
-      for (int i = 0; i < G::LIT; ++i) {
-        if (lsrc[i] == nullptr) continue;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ldst[i] + buf * UBUF),
-                     "l"(lsrc[i] + xoff) : "memory");
-      }
-    } else {
-      const bool xb = !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
-#pragma unroll
-      for (int i = 0; i < G::LIT; ++i) {
-        if (lsrc[i] == nullptr) continue;
-        const int nb = (xb || lbnd[i]) ? 0 : 8;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
-                     "l"(lsrc[i] + xoff), "r"(nb) : "memory");
-      }
+    for (int i = 0; i < G::LIT; ++i) {
+      if (LTAIL && i == G::LIT - 1 && tid + i * NT >= G::LITEMS) break;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
+                   "l"(base + loff[i]), "r"(xb ? 0u : lnb[i]) : "memory");
     }
     cp_async_commit();
   };
@@ -807,6 +789,8 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
   const int gz = (a.g.Ez + 1 + G::TZE - 1) / G::TZE;
   const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + G::TYE - 1) / G::TYE;
   const int nb = BLOCK ? a.nblk / Q : 1;  // CTA groups of Q blocks
+  // the plane loads address a CTA's Q stage rows with 32-bit offsets from its first row
+  if ((long long)(Q - 1) * a.su + a.g.n > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
   dim3 grid(gz, gy, a.nchunks * nb);
   if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
   kern<<<grid, G::NT, smem, s>>>(a);
