@@ -221,6 +221,31 @@ int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, in
   return SPK_OK;
 }
 
+// row range (x*ny + y) of the produced planes of a level and the row-kernel geometry
+SpkRowArgs row_args(const spk_ctx* c, int level) {
+  SpkRowArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = c->dims[level];
+  a.t = c->tabs[level];
+  int xb = 0, xe = a.g.nx;
+  if (a.g.Ex > 0) {
+    xb = c->K * c->ex_begin[level];
+    xe = c->K * c->ex_end[level] + ((c->store_last[level] && c->ex_end[level] == a.g.Ex) ? 1 : 0);
+  }
+  a.row0 = xb * a.g.ny;
+  a.nrows = (xe - xb) * a.g.ny;
+  int tpr = 1;
+  while (tpr < a.g.nz && tpr < 128) tpr *= 2;
+  a.tpr = tpr;
+  a.constrained = 1;
+  return a;
+}
+
+// the fused K1 Chebyshev epilogue is latency-bound on its global operands at large levels: there
+// the step runs as a K1 STORE of w = A d followed by the row-parallel update (more bytes, near the
+// HBM roofline); small (L2-resident) levels keep the single fused launch
+constexpr long long SPK_SPLIT_CHEB_MIN = 1LL << 20;
+
 }  // namespace
 
 extern "C" {
@@ -458,18 +483,16 @@ int spk_residual(spk_ctx* c, int level, int nblk, const double* lams, double tau
 int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* cs,
                   const double* b, double* r, double* x, double* d, void* stream) {
   if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
   for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
     const int nb = std::min(SPK_BMAX, nblk - b0);
-    SpkVecArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.g = c->dims[level];
-    a.t = c->tabs[level];
-    a.nblk = nb; a.blk_base = 0; a.constrained = 1; a.pair = 0; a.lam_uniform = 0;
+    SpkRowArgs a = row_args(c, level);
+    a.nblk = nb;
     a.tau = tau;
-    for (int i = 0; i < nb; ++i) { a.lam[i] = lams[b0 + i]; a.c[i] = cs[b0 + i]; }
-    const long long off = (long long)b0 * a.g.n;
-    a.in0 = b + off; a.out0 = r + off; a.out1 = x + off; a.out2 = d + off;
-    cudaError_t e = spk_launch_cheb_init(c->K, a, (cudaStream_t)stream);
+    for (int i = 0; i < nb; ++i) { a.lam[i] = lams[b0 + i]; a.c1[i] = cs[b0 + i]; }
+    const long long off = (long long)b0 * n;
+    a.b = b + off; a.r = r + off; a.x = x + off; a.d_out = d + off;
+    cudaError_t e = spk_launch_cheb_rows(c->K, 0, a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "cheb_init");
   }
   return SPK_OK;
@@ -480,6 +503,32 @@ int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double ta
                   int final_step, int* nan_flag, void* stream) {
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
+  if ((long long)nblk * n >= SPK_SPLIT_CHEB_MIN) {
+    // w = A d into d_out (constrained: boundary rows carry d), then the pointwise update
+    SpkApplyArgs ap = base_args(c, level);
+    ap.u = d_in; ap.su = n; ap.v = d_out; ap.sv = n;
+    if (int rc = apply_blocks_chunked(c, level, nblk, lams, 0, tau, 1, EPI_STORE, ap, (cudaStream_t)stream,
+                                      nullptr, nullptr))
+      return rc;
+    for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
+      const int nb = std::min(SPK_BMAX, nblk - b0);
+      SpkRowArgs a = row_args(c, level);
+      a.nblk = nb;
+      a.tau = tau;
+      a.final_step = final_step;
+      a.nan_flag = nan_flag;
+      for (int i = 0; i < nb; ++i) {
+        a.lam[i] = lams[b0 + i];
+        a.c1[i] = c1s[b0 + i];
+        a.c2[i] = c2s[b0 + i];
+      }
+      const long long off = (long long)b0 * n;
+      a.w = d_out + off; a.d = d_in + off; a.r = r + off; a.x = x + off; a.d_out = d_out + off;
+      cudaError_t e = spk_launch_cheb_rows(c->K, final_step ? 2 : 1, a, (cudaStream_t)stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cheb update");
+    }
+    return SPK_OK;
+  }
   SpkApplyArgs a = base_args(c, level);
   a.u = d_in; a.su = n; a.r = r; a.x = x; a.d_out = d_out; a.se = n;
   a.final_step = final_step; a.nan_flag = nan_flag;

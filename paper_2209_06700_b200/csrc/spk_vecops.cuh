@@ -17,6 +17,25 @@ struct SpkVecArgs {
   double* out2;
 };
 
+// row-parallel pointwise smoother kernels (one CTA row group per (x, y) line of nz nodes, all blocks):
+// Chebyshev start and the Chebyshev update that follows a K1 STORE of w = A d
+struct SpkRowArgs {
+  SpkDims g;
+  SpkTab t;
+  int nblk, constrained, final_step;
+  int row0, nrows;        // rows (x*ny + y) [row0, row0 + nrows): the owned planes of a slab window
+  int tpr;                // threads per row (power of two, <= blockDim)
+  double lam[SPK_BMAX], c1[SPK_BMAX], c2[SPK_BMAX];
+  double tau;
+  const double* w;        // update: A d
+  const double* d;        // update: previous direction
+  const double* b;        // init: right-hand side
+  double* r;
+  double* x;
+  double* d_out;
+  int* nan_flag;
+};
+
 struct SpkTransferArgs {
   const double* in;
   double* out;
@@ -71,6 +90,7 @@ struct SpkRhsArgs {
 
 cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s);
 cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s);
+cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s);
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s);
 int spk_mgs_grid();

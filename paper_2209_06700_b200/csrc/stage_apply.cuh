@@ -23,6 +23,10 @@
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
 
+#ifndef SPK_MINB_ALL
+#define SPK_MINB_ALL 1
+#endif
+
 namespace {
 
 template <int K> struct Tile;
@@ -346,7 +350,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
 }
 
 template <int K, int Q, bool BLOCK, int EPI>
-__global__ void __launch_bounds__(Geo<K, Q>::NT, (EPI == EPI_STORE || Q <= 2) ? Geo<K, Q>::MINB : 1)
+__global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB : ((EPI == EPI_STORE || Q <= 2) ? Geo<K, Q>::MINB : 1))
     stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
   using G = Geo<K, Q>;
   constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;

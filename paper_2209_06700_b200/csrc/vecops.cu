@@ -157,6 +157,60 @@ __global__ void transfer_axis_kernel(const __grid_constant__ SpkTransferArgs a) 
   }
 }
 
+
+// ---- row-parallel Chebyshev kernels: op 0 start (r = b, x = 0, d = Dinv r / theta),
+//      op 1 update after w = A d (r -= w; x += d; d = c1 d + c2 Dinv r), op 2 = op 1 fused with the
+//      final "return x + d" (multigrid.py:82-88) + NaN flag. The Jacobi diagonal is recomputed from the
+//      node class (row-uniform x/y factors, per-node z factor); no index divisions per node.
+template <int K, int OP>
+__global__ void __launch_bounds__(128) cheb_rows_kernel(const __grid_constant__ SpkRowArgs a) {
+  const SpkDims& g = a.g;
+  const int rpc = blockDim.x / a.tpr;  // rows per CTA
+  const int row = a.row0 + blockIdx.x * rpc + threadIdx.x / a.tpr;
+  if (row >= a.row0 + a.nrows) return;
+  const int x = row / g.ny, y = row - x * g.ny;
+  double mx, kx, my, ky;
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], x + g.x0, g.Exg, mx, kx);
+  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], y, g.Ey, my, ky);
+  const bool bxy = a.constrained && ((g.Ex > 0 && (x + g.x0 <= 0 || x + g.x0 >= g.nxg - 1)) ||
+                                     (g.Ey > 0 && (y == 0 || y == g.ny - 1)));
+  const long long base = (long long)row * g.nz;
+  bool bad = false;
+  for (int z = threadIdx.x % a.tpr; z < g.nz; z += a.tpr) {
+    const bool bnd = bxy || (a.constrained && g.Ez > 0 && (z == 0 || z == g.nz - 1));
+    double mz, kz;
+    dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], z, g.Ez, mz, kz);
+    const double dm = (mx * my) * mz;
+    const double dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+    const long long i0 = base + z;
+    for (int b = 0; b < a.nblk; ++b) {
+      const long long i = (long long)b * g.n + i0;
+      const double inv = bnd ? 1.0 : 1.0 / (a.lam[b] * dm + a.tau * dk);
+      if constexpr (OP == 0) {
+        const double r = a.b[i];
+        a.r[i] = r;
+        a.x[i] = 0.0;
+        a.d_out[i] = (inv * r) / a.c1[b];
+      } else {
+        const double dq = a.d[i];
+        const double rn = a.r[i] - a.w[i];
+        const double xq = a.x[i] + dq;
+        const double dn = a.c1[b] * dq + a.c2[b] * (inv * rn);
+        if constexpr (OP == 1) {
+          a.r[i] = rn;
+          a.x[i] = xq;
+          a.d_out[i] = dn;
+        } else {
+          const double xn = xq + dn;
+          a.x[i] = xn;
+          bad |= !isfinite(xn);
+        }
+      }
+    }
+  }
+  if (OP == 2 && bad && a.nan_flag) atomicOr(a.nan_flag, 1);
+}
+
 // ---- (D (x) I) u : out_i = sum_j D_ij in_j (pointwise, all stages in registers) ----
 __global__ void combine_kernel(const __grid_constant__ SpkCombineArgs a) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
@@ -383,6 +437,27 @@ cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s)
     case 4: transfer_axis_kernel<4><<<nb, TPB, 0, s>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s) {
+  const int rpc = 128 / a.tpr;
+  const int nb = (a.nrows + rpc - 1) / rpc;
+  if (nb <= 0) return cudaSuccess;
+#define SPK_ROWS(KK)                                                                   \
+  switch (op) {                                                                        \
+    case 0: cheb_rows_kernel<KK, 0><<<nb, 128, 0, s>>>(a); break;                     \
+    case 1: cheb_rows_kernel<KK, 1><<<nb, 128, 0, s>>>(a); break;                     \
+    default: cheb_rows_kernel<KK, 2><<<nb, 128, 0, s>>>(a); break;                    \
+  }
+  switch (K) {
+    case 1: SPK_ROWS(1) break;
+    case 2: SPK_ROWS(2) break;
+    case 3: SPK_ROWS(3) break;
+    case 4: SPK_ROWS(4) break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef SPK_ROWS
   return cudaGetLastError();
 }
 
