@@ -6,6 +6,7 @@
 //     (krylov.py:74-82), device-resident Hessenberg entries (no host round trip per dot)
 //   * RHS assembly for separable sources and nodal interpolation (fem.py:220-246, :368-372)
 #include <cmath>
+#include <cstdint>
 
 #include "spk_internal.cuh"
 #include "spk_vecops.cuh"
@@ -269,43 +270,87 @@ __device__ void finalize_partials(double mine, double* partial, unsigned* counte
 }
 
 // ---- MGS step: w -= h_prev * v_prev ; out = <v_cur, w> (or ||w|| if v_cur == null) ----
-__global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
-  // 4 independent elements per thread and iteration keep enough loads in flight to stream HBM
-  __shared__ double red[TPB];
+// Streams 2-3 vectors: every thread first issues all its loads (16-byte accesses when the three
+// vectors share 16-byte alignment, 4 independent pairs per iteration), then updates and reduces.
+template <bool PREV, bool CUR>
+__device__ __forceinline__ double mgs_body(const SpkMgsArgs& a, double h) {
+  double* __restrict__ w = a.w;
+  const double* __restrict__ vp = a.v_prev;
+  const double* __restrict__ vc = a.v_cur;
+  const long long n = a.n;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  const double h = a.v_prev ? *a.h_prev : 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long i = base;
-  for (; i + 3 * stride < a.n; i += 4 * stride) {
-    double w[4], c[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) w[u] = a.w[i + u * stride];
-    if (a.v_prev) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        w[u] = w[u] - h * a.v_prev[i + u * stride];
-        a.w[i + u * stride] = w[u];
+  // (read-only sweeps stream best with scalar accesses; the update sweep with 16-byte ones)
+  const bool vec = PREV && ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(vp) |
+                             (CUR ? reinterpret_cast<uintptr_t>(vc) : 0)) & 15) == 0;
+  long long done = 0;
+  if (vec) {
+    const long long n2 = n / 2;
+    double2* __restrict__ w2 = reinterpret_cast<double2*>(w);
+    const double2* __restrict__ p2 = reinterpret_cast<const double2*>(vp);
+    const double2* __restrict__ c2 = reinterpret_cast<const double2*>(vc);
+    long long i = tid;
+    for (; i + nth < n2; i += 2 * nth) {
+      double2 wa = w2[i], wb = w2[i + nth];
+      double2 pa, pb, ca, cb;
+      if (PREV) { pa = __ldcs(p2 + i); pb = __ldcs(p2 + i + nth); }
+      if (CUR) { ca = c2[i]; cb = c2[i + nth]; }
+      if (PREV) {
+        wa.x = wa.x - h * pa.x; wa.y = wa.y - h * pa.y;
+        wb.x = wb.x - h * pb.x; wb.y = wb.y - h * pb.y;
+        w2[i] = wa;
+        w2[i + nth] = wb;
       }
+      if (!CUR) { ca = wa; cb = wb; }
+      s0 = fma(ca.x, wa.x, s0); s1 = fma(ca.y, wa.y, s1);
+      s2 = fma(cb.x, wb.x, s2); s3 = fma(cb.y, wb.y, s3);
     }
+    for (; i < n2; i += nth) {
+      double2 wa = w2[i];
+      if (PREV) {
+        const double2 pa = __ldcs(p2 + i);
+        wa.x = wa.x - h * pa.x; wa.y = wa.y - h * pa.y;
+        w2[i] = wa;
+      }
+      const double2 ca = CUR ? c2[i] : wa;
+      s0 = fma(ca.x, wa.x, s0); s1 = fma(ca.y, wa.y, s1);
+    }
+    done = 2 * n2;
+  }
+  long long i = done + tid;
+  if (!PREV) {  // 4 independent elements per thread and iteration
+    for (; i + 3 * nth < n; i += 4 * nth) {
+      double wv[4], c[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) c[u] = a.v_cur ? a.v_cur[i + u * stride] : w[u];
-    s0 = fma(c[0], w[0], s0);
-    s1 = fma(c[1], w[1], s1);
-    s2 = fma(c[2], w[2], s2);
-    s3 = fma(c[3], w[3], s3);
-  }
-  for (; i < a.n; i += stride) {
-    double w = a.w[i];
-    if (a.v_prev) {
-      w = w - h * a.v_prev[i];
-      a.w[i] = w;
+      for (int u = 0; u < 4; ++u) wv[u] = w[i + u * nth];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = CUR ? vc[i + u * nth] : wv[u];
+      s0 = fma(c[0], wv[0], s0);
+      s1 = fma(c[1], wv[1], s1);
+      s2 = fma(c[2], wv[2], s2);
+      s3 = fma(c[3], wv[3], s3);
     }
-    const double c = a.v_cur ? a.v_cur[i] : w;
-    s0 = fma(c, w, s0);
   }
-  const double mine = block_sum((s0 + s1) + (s2 + s3), red);
-  finalize_partials(mine, a.partial, a.counter, a.out, a.v_cur == nullptr, red);
+  for (; i < n; i += nth) {
+    double wv = w[i];
+    if (PREV) {
+      wv = wv - h * vp[i];
+      w[i] = wv;
+    }
+    const double c = CUR ? vc[i] : wv;
+    s0 = fma(c, wv, s0);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+__global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
+  __shared__ double red[TPB];
+  const double h = a.v_prev ? *a.h_prev : 0.0;
+  double mine;
+  if (a.v_prev) mine = a.v_cur ? mgs_body<true, true>(a, h) : mgs_body<true, false>(a, h);
+  else mine = a.v_cur ? mgs_body<false, true>(a, h) : mgs_body<false, false>(a, h);
+  finalize_partials(block_sum(mine, red), a.partial, a.counter, a.out, a.v_cur == nullptr, red);
 }
 
 // ---- v = w / *h ----
