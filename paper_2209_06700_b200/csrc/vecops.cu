@@ -235,6 +235,65 @@ __global__ void combine_kernel(const __grid_constant__ SpkCombineArgs a) {
   }
 }
 
+// small combines (NIN, NOUT <= 4: the stage transforms of Q <= 4 and their paired forms) with
+// compile-time sizes: two independent nodes per thread, all loads first, no read of out unless
+// accumulating
+template <int NIN, int NOUT, bool ACC, bool MASK>
+__global__ void __launch_bounds__(TPB) combine_small_kernel(const __grid_constant__ SpkCombineArgs a) {
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n; i += 2 * nth) {
+    const bool two = i + nth < a.n;
+    double in0[NIN], in1[NIN];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) {
+      in0[j] = a.in[j][i];
+      in1[j] = two ? a.in[j][i + nth] : 0.0;
+    }
+    bool b0 = false, b1 = false;
+    if (MASK) {
+      int x, y, z;
+      decompose(i, a.g, x, y, z);
+      b0 = bnd3(a.g, x, y, z);
+      if (two) {
+        decompose(i + nth, a.g, x, y, z);
+        b1 = bnd3(a.g, x, y, z);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) {
+        s0 = fma(a.D[o * SPK_CMAX + j], in0[j], s0);
+        s1 = fma(a.D[o * SPK_CMAX + j], in1[j], s1);
+      }
+      if (MASK) {
+        if (b0) s0 = 0.0;
+        if (b1) s1 = 0.0;
+      }
+      double* out = a.out + o * a.sout;
+      if (ACC) {
+        s0 += out[i];
+        if (two) s1 += out[i + nth];
+      }
+      out[i] = s0;
+      if (two) out[i + nth] = s1;
+    }
+  }
+}
+
+template <int NIN, int NOUT>
+cudaError_t launch_small(const SpkCombineArgs& a, cudaStream_t s, int nb) {
+  if (a.accumulate) {
+    if (a.mask) combine_small_kernel<NIN, NOUT, true, true><<<nb, TPB, 0, s>>>(a);
+    else combine_small_kernel<NIN, NOUT, true, false><<<nb, TPB, 0, s>>>(a);
+  } else {
+    if (a.mask) combine_small_kernel<NIN, NOUT, false, true><<<nb, TPB, 0, s>>>(a);
+    else combine_small_kernel<NIN, NOUT, false, false><<<nb, TPB, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 // ---- deterministic block reduction helper ----
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int tid = threadIdx.x;
@@ -507,6 +566,13 @@ cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_
 }
 
 cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s) {
+  const int nb = grid_for((a.n + 1) / 2);
+#define SPK_CS(I, O) if (a.nin == I && a.nout == O) return launch_small<I, O>(a, s, nb);
+  SPK_CS(1, 1) SPK_CS(1, 2) SPK_CS(1, 3) SPK_CS(1, 4)
+  SPK_CS(2, 1) SPK_CS(2, 2) SPK_CS(2, 3) SPK_CS(2, 4)
+  SPK_CS(3, 1) SPK_CS(3, 2) SPK_CS(3, 3) SPK_CS(3, 4)
+  SPK_CS(4, 1) SPK_CS(4, 2) SPK_CS(4, 3) SPK_CS(4, 4)
+#undef SPK_CS
   combine_kernel<<<grid_for(a.n), TPB, 0, s>>>(a);
   return cudaGetLastError();
 }
