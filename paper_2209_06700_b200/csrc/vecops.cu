@@ -102,62 +102,89 @@ __global__ void axpy_flag_kernel(long long total, double* x, const double* d, in
 }
 
 // ---- one-axis transfer: view arrays as [outer][n_axis][inner] ----
+// one output node of a 1D transfer sweep: src points at the input column (stride `inner`),
+// indexed by GLOBAL node number along the swept axis (local = global - in_off)
 template <int K>
-__global__ void transfer_axis_kernel(const __grid_constant__ SpkTransferArgs a) {
-  constexpr int P2 = 2 * SPK_KMAX + 1;
-  const long long total = a.outer * (long long)a.nout * a.inner;
-  for (long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x; gid < total;
-       gid += (long long)gridDim.x * blockDim.x) {
-    const long long in_idx = gid % a.inner;
-    const long long rest = gid / a.inner;
-    const int il = a.o_begin + (int)(rest % a.nout);  // local output node
-    const int i = il + a.out_off;                      // global output node
-    const long long o = rest / a.nout;
-    // input rows are addressed by global node index (local = global - in_off)
-    const double* src = a.in + o * (long long)a.nin * a.inner + in_idx - (long long)a.in_off * a.inner;
-    double val = 0.0;
-    if (a.prolong) {
-      // fine node i <- coarse element ec, local fine position f in [0, 2K]
-      const int Nc = a.Nc;
-      const int ec = min(i / (2 * K), Nc - 1);
-      const int f = i - 2 * K * ec;
+__device__ __forceinline__ double transfer_value(const SpkTransferArgs& a, int i, const double* src,
+                                                 long long inner) {
+  double val = 0.0;
+  const int Nc = a.Nc;
+  if (a.prolong) {
+    // fine node i <- coarse element ec, local fine position f in [0, 2K]
+    const int ec = min(i / (2 * K), Nc - 1);
+    const int f = i - 2 * K * ec;
 #pragma unroll
-      for (int j = 0; j <= K; ++j) val = fma(a.P[f * (SPK_KMAX + 1) + j], src[(long long)(K * ec + j) * a.inner], val);
+    for (int j = 0; j <= K; ++j) val = fma(a.P[f * (SPK_KMAX + 1) + j], src[(long long)(K * ec + j) * inner], val);
+  } else {
+    // coarse node J = K*ec + r gathers P^T
+    const int ec = i / K, r = i - ec * K;
+    if (r != 0) {
+#pragma unroll
+      for (int f = 1; f < 2 * K; ++f)
+        val = fma(a.P[f * (SPK_KMAX + 1) + r], src[(long long)(2 * K * ec + f) * inner], val);
     } else {
-      // coarse node J = K*ec + r gathers P^T
-      const int Nc = a.Nc;
-      const int ec = i / K, r = i - ec * K;
-      if (r != 0) {
+      val = src[(long long)(2 * K * ec) * inner];  // coincident fine vertex, weight 1
+      if (ec < Nc) {
 #pragma unroll
         for (int f = 1; f < 2 * K; ++f)
-          val = fma(a.P[f * (SPK_KMAX + 1) + r], src[(long long)(2 * K * ec + f) * a.inner], val);
-      } else {
-        val = src[(long long)(2 * K * ec) * a.inner];  // coincident fine vertex, weight 1
-        if (ec < Nc) {
+          val = fma(a.P[f * (SPK_KMAX + 1) + 0], src[(long long)(2 * K * ec + f) * inner], val);
+      }
+      if (ec > 0) {
 #pragma unroll
-          for (int f = 1; f < 2 * K; ++f)
-            val = fma(a.P[f * (SPK_KMAX + 1) + 0], src[(long long)(2 * K * ec + f) * a.inner], val);
-        }
-        if (ec > 0) {
-#pragma unroll
-          for (int f = 1; f < 2 * K; ++f)
-            val = fma(a.P[f * (SPK_KMAX + 1) + K], src[(long long)(2 * K * (ec - 1) + f) * a.inner], val);
-        }
+        for (int f = 1; f < 2 * K; ++f)
+          val = fma(a.P[f * (SPK_KMAX + 1) + K], src[(long long)(2 * K * (ec - 1) + f) * inner], val);
       }
     }
-    (void)P2;
-    const long long oidx = (o * (long long)a.onodes + il) * a.inner + in_idx;
-    if (a.mask) {
-      const long long gi = oidx % a.g.n;
-      int x, y, z;
-      decompose(gi, a.g, x, y, z);
-      if (bnd3(a.g, x, y, z)) val = 0.0;
-    }
-    if (a.accumulate) a.out[oidx] += val;
-    else a.out[oidx] = val;
+  }
+  return val;
+}
+
+// sweep along the contiguous (z) axis: one CTA per input row, threads along the output row
+template <int K>
+__global__ void __launch_bounds__(128) transfer_rows_kernel(const __grid_constant__ SpkTransferArgs a) {
+  const long long o = blockIdx.x;
+  const double* src = a.in + o * (long long)a.nin - a.in_off;
+  int x = 0, y = 0;
+  if (a.mask) {  // final sweep of a 1D hierarchy: the row is (x, y) of the output level
+    y = (int)(o % a.g.ny);
+    x = (int)((o / a.g.ny) % a.g.nx);
+  }
+  for (int il = a.o_begin + threadIdx.x; il < a.o_begin + a.nout; il += blockDim.x) {
+    double val = transfer_value<K>(a, il + a.out_off, src, 1);
+    if (a.mask && bnd3(a.g, x, y, il)) val = 0.0;
+    double* dst = a.out + o * (long long)a.onodes + il;
+    if (a.accumulate) val += *dst;
+    *dst = val;
   }
 }
 
+// sweep along a strided axis (y: inner = nz, x: inner = ny*nz): grid (inner chunks, output node,
+// outer row), threads along the contiguous inner index -- no index division per element
+template <int K>
+__global__ void __launch_bounds__(256) transfer_cols_kernel(const __grid_constant__ SpkTransferArgs a) {
+  const long long in_idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (in_idx >= a.inner) return;
+  const int il = a.o_begin + (int)blockIdx.y;
+  const long long o = blockIdx.z;
+  const double* src = a.in + o * (long long)a.nin * a.inner + in_idx - (long long)a.in_off * a.inner;
+  double val = transfer_value<K>(a, il + a.out_off, src, a.inner);
+  if (a.mask) {  // final sweep: x-axis of a 3D level, or y-axis of a 2D level
+    int x, y, z;
+    if (a.g.Ex > 0) {
+      x = il;
+      y = (int)(in_idx / a.g.nz);
+      z = (int)(in_idx - (long long)y * a.g.nz);
+    } else {
+      x = 0;
+      y = il;
+      z = (int)in_idx;
+    }
+    if (bnd3(a.g, x, y, z)) val = 0.0;
+  }
+  double* dst = a.out + (o * (long long)a.onodes + il) * a.inner + in_idx;
+  if (a.accumulate) val += *dst;
+  *dst = val;
+}
 
 // ---- row-parallel Chebyshev kernels: op 0 start (r = b, x = 0, d = Dinv r / theta),
 //      op 1 update after w = A d (r -= w; x += d; d = c1 d + c2 Dinv r), op 2 = op 1 fused with the
@@ -532,14 +559,26 @@ cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, in
 }
 
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s) {
-  const long long total = a.outer * (long long)a.nout * a.inner;
-  const int nb = grid_for(total);
-  switch (K) {
-    case 1: transfer_axis_kernel<1><<<nb, TPB, 0, s>>>(a); break;
-    case 2: transfer_axis_kernel<2><<<nb, TPB, 0, s>>>(a); break;
-    case 3: transfer_axis_kernel<3><<<nb, TPB, 0, s>>>(a); break;
-    case 4: transfer_axis_kernel<4><<<nb, TPB, 0, s>>>(a); break;
-    default: return cudaErrorInvalidValue;
+  if (a.nout <= 0 || a.outer <= 0) return cudaSuccess;
+  if (a.inner == 1) {
+    const unsigned nb = (unsigned)a.outer;
+    switch (K) {
+      case 1: transfer_rows_kernel<1><<<nb, 128, 0, s>>>(a); break;
+      case 2: transfer_rows_kernel<2><<<nb, 128, 0, s>>>(a); break;
+      case 3: transfer_rows_kernel<3><<<nb, 128, 0, s>>>(a); break;
+      case 4: transfer_rows_kernel<4><<<nb, 128, 0, s>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    if (a.outer > 65535 || a.nout > 65535) return cudaErrorInvalidValue;
+    dim3 grid((unsigned)((a.inner + 255) / 256), (unsigned)a.nout, (unsigned)a.outer);
+    switch (K) {
+      case 1: transfer_cols_kernel<1><<<grid, 256, 0, s>>>(a); break;
+      case 2: transfer_cols_kernel<2><<<grid, 256, 0, s>>>(a); break;
+      case 3: transfer_cols_kernel<3><<<grid, 256, 0, s>>>(a); break;
+      case 4: transfer_cols_kernel<4><<<grid, 256, 0, s>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
   }
   return cudaGetLastError();
 }
