@@ -260,21 +260,26 @@ __device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 
 template <int K, int Q, bool BLOCK, int EPI>
 __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q],
                                          const double* dtab, const double (&ith)[Q], int x, int y, int z,
-                                         const double (&val)[Q], double& sumsq) {
+                                         long long gi, const double (&val)[Q], double& sumsq) {
+  // gi: node index of (x, y, z) in the level (x * ny*nz + y * nz + z), precomputed by the caller
   const SpkDims& g = a.g;
-  const long long gi = ((long long)x * g.ny + y) * g.nz + z;
-  const bool bnd = a.constrained && on_boundary(g, x, y, z);
-  const long long ubase = BLOCK ? (long long)b0 * a.su : 0;
-  const long long ebase = BLOCK ? (long long)b0 * a.se : 0;
-  const long long vbase = BLOCK ? (long long)b0 * a.sv : 0;
+  const long long ubase = (BLOCK ? (long long)b0 * a.su : 0) + gi;
+  const long long ebase = (BLOCK ? (long long)b0 * a.se : 0) + gi;
+  const long long vbase = (BLOCK ? (long long)b0 * a.sv : 0) + gi;
   const int slot0 = BLOCK ? b0 - a.blk_base : 0;
+  const bool bnd = a.constrained && on_boundary(g, x, y, z);
   double Av[Q];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) Av[q] = bnd ? __ldg(a.u + ubase + q * a.su + gi) : val[q];
+  for (int q = 0; q < Q; ++q) Av[q] = val[q];
+  if (bnd) {  // constrained boundary rows are the identity (rare: a real branch, not a select)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) Av[q] = __ldg(a.u + ubase + q * a.su);
+  }
 
   if constexpr (EPI == EPI_STORE) {
+    double* vp = a.v + vbase;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) __stcs(a.v + vbase + q * a.sv + gi, Av[q]);
+    for (int q = 0; q < Q; ++q) __stcs(vp + q * a.sv, Av[q]);
   } else {
     // Jacobi diagonal (reference operator_diagonal fem.py:172-187, 1.0 on boundary): looked up in
     // the per-CTA table of node classes (no per-node division)
@@ -293,30 +298,35 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
         if constexpr (Q > 1) z0[1] = -B_ * rr[0] + A_ * rr[1];
       }
     };
+    double* rp = a.r + ebase;
+    double* xp = a.x + ebase;
     if constexpr (EPI == EPI_DINV) {
       jacobi(Av);
+      double* vp = a.v + vbase;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        a.v[vbase + q * a.sv + gi] = z0[q];
+        vp[q * a.sv] = z0[q];
         sumsq = fma(z0[q], z0[q], sumsq);
       }
     } else {
-      double rn[Q], xfin[Q];
+      double rn[Q], xfin[Q], dq[Q];
       if constexpr (EPI == EPI_RESID) {
+        const double* bp = a.b + ebase;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          rn[q] = __ldg(a.b + ebase + q * a.se + gi) - Av[q];
-          a.r[ebase + q * a.se + gi] = rn[q];
+          rn[q] = __ldg(bp + q * a.se) - Av[q];
+          rp[q * a.se] = rn[q];
         }
       } else {  // EPI_CHEB:  x += d ; r -= A d ; d = c1 d + c2 Dinv r   (multigrid.py:82-87)
+        const double* up = a.u + ubase;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const double dq = __ldg(a.u + ubase + q * a.su + gi);
-          rn[q] = a.r[ebase + q * a.se + gi] - Av[q];
-          const double xq = a.x[ebase + q * a.se + gi] + dq;
+          dq[q] = __ldg(up + q * a.su);
+          rn[q] = rp[q * a.se] - Av[q];
+          const double xq = xp[q * a.se] + dq[q];
           if (!a.final_step) {
-            a.r[ebase + q * a.se + gi] = rn[q];
-            a.x[ebase + q * a.se + gi] = xq;
+            rp[q * a.se] = rn[q];
+            xp[q * a.se] = xq;
           } else {
             xfin[q] = xq;
           }
@@ -325,23 +335,23 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
       if (a.d_out != nullptr) {
         jacobi(rn);
         bool bad = false;
+        double* dp = a.d_out + ebase;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int slot = BLOCK ? slot0 + q : 0;
           double dn;
           if constexpr (EPI == EPI_CHEB) {
-            const double dq = __ldg(a.u + ubase + q * a.su + gi);
-            dn = a.c1[slot] * dq + a.c2[slot] * z0[q];
+            dn = a.c1[slot] * dq[q] + a.c2[slot] * z0[q];
             if (a.final_step) {  // last step fused with "return x + d" (multigrid.py:88) + NaN check
               const double xn = xfin[q] + dn;
-              a.x[ebase + q * a.se + gi] = xn;
+              xp[q * a.se] = xn;
               bad |= !isfinite(xn);
               continue;
             }
           } else {
             dn = z0[q] * ith[q];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
           }
-          a.d_out[ebase + q * a.se + gi] = dn;
+          dp[q * a.se] = dn;
         }
         if (bad && a.nan_flag) atomicOr(a.nan_flag, 1);
       }
@@ -607,13 +617,14 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 
   // X-phase state
   double acc[PPT][Q][K + 1];
-  int pyl[PPT], pzl[PPT];
+  int pyl[PPT], pzl[PPT], pyz[PPT];
   bool pv[PPT];
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
     const int p = tid + j * NT;
     pyl[j] = p / TZ;
     pzl[j] = p - pyl[j] * TZ;
+    pyz[j] = (y_lo + pyl[j]) * g.nz + (z_lo + pzl[j]);
     pv[j] = (p < TY * TZ) && pyl[j] < nyo && pzl[j] < nzo;
 #pragma unroll
     for (int q = 0; q < Q; ++q)
@@ -683,7 +694,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
       }
       const int y = y_lo + yl, z = z_lo + zl;
       if (xdeg) {
-        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, 0, y, z, pq, sumsq);
+        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, 0, y, z, (long long)pyz[j], pq, sumsq);
         continue;
       }
 #pragma unroll
@@ -698,14 +709,17 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
             double val[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
-            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * ecur + s, y, z, val, sumsq);
+            const int xx = K * ecur + s;
+            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, xx, y, z,
+                                       (long long)xx * plane_stride + pyz[j], val, sumsq);
           }
         }
         if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
           double val[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
-          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * g.Ex, y, z, val, sumsq);
+          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
+                                     (long long)(K * g.Ex) * plane_stride + pyz[j], val, sumsq);
         }
         // carry the shared vertex and start the next element with this plane as its local 0
 #pragma unroll
