@@ -126,6 +126,9 @@ template <int K> struct Coef {
 };
 
 template <int V> struct IC { static constexpr int value = V; };
+// plane-buffer parity: a compile-time IC<p> (unrolled pipeline) or a runtime int
+template <int V> __device__ __forceinline__ constexpr int parity_of(IC<V>) { return V; }
+__device__ __forceinline__ int parity_of(int v) { return v; }
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -455,7 +458,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
-  auto load_plane = [&](int x, int buf) {
+  auto load_plane = [&](int x, auto BUF) {
+    const unsigned buf = parity_of(BUF);
     const double* base = u + (long long)x * plane_stride;
     // constrained: the x-boundary planes are zero (uniform per plane)
     const bool xb = a.constrained && !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
@@ -518,7 +522,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   }
 
   // ---------------- Z-phase: A = Mz u, B = Kz u ----------------
-  auto zphase = [&](int ub, int ab) {
+  auto zphase = [&](auto PB) {
+    const int ub = parity_of(PB), ab = ub;
     const double* Ub = Us + ub * G::U_SZ;
     double* As = ABs + ab * 2 * G::AB_SZ;
     double* Bs = As + G::AB_SZ;
@@ -557,7 +562,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   };
 
   // ---------------- Y-phase: MA = My A, C = Ky A + My B ----------------
-  auto yphase = [&](int ab, int mc) {
+  auto yphase = [&](auto PB) {
+    const int ab = parity_of(PB), mc = ab;
     const double* As = ABs + ab * 2 * G::AB_SZ;
     const double* Bs = As + G::AB_SZ;
     double* MAs = MCs + mc * 2 * G::MC_SZ;
@@ -637,7 +643,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   // ---------------- X-phase: stage mix + element-push accumulation ----------------
   // the plane's local index r within element ecur is uniform: dispatch to a copy with the x-table
   // column as compile-time register operands
-  auto xphase_r = [&](auto RC, int x, int mc) {
+  auto xphase_r = [&](auto RC, int x, auto MC) {
+    const int mc = parity_of(MC);
     constexpr int RR = decltype(RC)::value;
     const double* MAs = MCs + mc * 2 * G::MC_SZ;
     const double* Cs = MAs + G::MC_SZ;
@@ -733,7 +740,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     }
     if (!xdeg && r_loc == K) ++ecur;
   };
-  auto xphase = [&](int x, int mc) {
+  auto xphase = [&](int x, auto mc) {
     const int r_loc = xdeg ? 0 : x - K * ecur;   // 0..K
     switch (r_loc) {
       case 0: xphase_r(IC<0>{}, x, mc); break;
@@ -744,35 +751,37 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     }
   };
 
-  if constexpr (G::PIPE3) {
-    // Three-stage software pipeline, ONE barrier per plane: interval t runs Z(t), Y(t-1), X(t-2)
-    // on disjoint double buffers (U/AB/MC indexed by plane parity) while U(t+1) is in flight.
-    load_plane(xs, 0);
-    for (int t = 0; t < nplanes + 2; ++t) {
-      cp_async_wait_all();
-      __syncthreads();
-      if (t + 1 < nplanes) load_plane(xs + t + 1, (t + 1) & 1);
-      if (t < nplanes) zphase(t & 1, t & 1);
-      if (t >= 1 && t - 1 < nplanes) yphase((t - 1) & 1, (t - 1) & 1);
-      if (t >= 2) xphase(xs + t - 2, t & 1);
-    }
-  } else {
-    // Two barriers per plane: Z(x+1) and X(x) share an interval (U/AB vs MC), Y(x+1) follows.
-    load_plane(xs, 0);
+  // Three-stage software pipeline, ONE barrier per plane: interval t runs Z(t), Y(t-1), X(t-2) on
+  // disjoint double buffers (U/AB/MC indexed by plane parity) while U(t+1) is in flight. The loop is
+  // unrolled by two so every buffer address is a compile-time offset.
+  auto interval = [&](auto P, int t) {
+    constexpr int p = decltype(P)::value;  // == t & 1
     cp_async_wait_all();
     __syncthreads();
-    zphase(0, 0);
-    if (nplanes > 1) load_plane(xs + 1, 1);
-    __syncthreads();
-    yphase(0, 0);
-    for (int pl = 0; pl < nplanes; ++pl) {
+    if (t + 1 < nplanes) load_plane(xs + t + 1, IC<1 - p>{});
+    if (t < nplanes) zphase(IC<p>{});
+    if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{});
+    if (t >= 2) xphase(xs + t - 2, IC<p>{});
+  };
+  load_plane(xs, IC<0>{});
+  // unroll the plane loop by two (compile-time buffer offsets); measured on B200 to help every
+  // instantiation except the stage-coupled k=2, Q=4 mix (C4's GMRES operator), whose doubled code
+  // is slower (623 vs 575 us)
+  constexpr bool UNROLL2 = BLOCK || !(K == 2 && Q == 4);
+  if constexpr (UNROLL2) {
+    for (int t = 0; t < nplanes + 2; t += 2) {
+      interval(IC<0>{}, t);
+      if (t + 1 < nplanes + 2) interval(IC<1>{}, t + 1);
+    }
+  } else {  // one copy of the interval with runtime buffer parity (smaller code)
+    for (int t = 0; t < nplanes + 2; ++t) {
+      const int p = t & 1;
       cp_async_wait_all();
-      __syncthreads();                     // U(x+1) landed; MC(x) ready; AB consumed
-      if (pl + 2 < nplanes) load_plane(xs + pl + 2, pl & 1);
-      if (pl + 1 < nplanes) zphase((pl + 1) & 1, 0);
-      xphase(xs + pl, 0);
-      __syncthreads();                     // AB(x+1) ready; MC(x) consumed
-      if (pl + 1 < nplanes) yphase(0, 0);
+      __syncthreads();
+      if (t + 1 < nplanes) load_plane(xs + t + 1, 1 - p);
+      if (t < nplanes) zphase(p);
+      if (t >= 1 && t - 1 < nplanes) yphase(1 - p);
+      if (t >= 2) xphase(xs + t - 2, p);
     }
   }
 
