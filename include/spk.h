@@ -126,6 +126,16 @@ int spk_ipc_open(const void* handle64, void** dev_ptr);
 int spk_ipc_close(void* dev_ptr);
 int spk_ipc_free(void* dev_ptr);
 int spk_copy_d2d(void* dst, const void* src, long long bytes, void* stream);
+/* Chebyshev from a zero start without materialising r = b, x = 0 (large levels, see spk_cheb_split):
+ * spk_cheb_start: d = Dinv b / theta; spk_cheb_first_step: w = A d (into d_out), r = b - w, x = d,
+ * d_out = c1 d + c2 Dinv r (final_step: x = d + d_new only, NaN flag) */
+int spk_cheb_start(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* thetas,
+                   const double* b, double* d, void* stream);
+int spk_cheb_first_step(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* c1s,
+                        const double* c2s, const double* b, const double* d_in, double* r, double* x,
+                        double* d_out, int final_step, int* nan_flag, void* stream);
+/* 1 if the Chebyshev steps of this level run split (K1 STORE + pointwise update), 0 if fused */
+int spk_cheb_split(spk_ctx* ctx, int level, int nblk);
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
             const double* v_cur, double* out, void* stream);
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);

@@ -498,6 +498,59 @@ int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double ta
   return SPK_OK;
 }
 
+int spk_cheb_start(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* thetas,
+                   const double* b, double* d, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
+    const int nb = std::min(SPK_BMAX, nblk - b0);
+    SpkRowArgs a = row_args(c, level);
+    a.nblk = nb;
+    a.tau = tau;
+    for (int i = 0; i < nb; ++i) { a.lam[i] = lams[b0 + i]; a.c1[i] = thetas[b0 + i]; }
+    const long long off = (long long)b0 * n;
+    a.b = b + off; a.d_out = d + off;
+    cudaError_t e = spk_launch_cheb_rows(c->K, 3, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cheb_start");
+  }
+  return SPK_OK;
+}
+
+int spk_cheb_first_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
+                        const double* c2s, const double* b, const double* d_in, double* r, double* x,
+                        double* d_out, int final_step, int* nan_flag, void* stream) {
+  if (int rc = check_level(c, level)) return rc;
+  const long long n = c->dims[level].n;
+  SpkApplyArgs ap = base_args(c, level);
+  ap.u = d_in; ap.su = n; ap.v = d_out; ap.sv = n;
+  if (int rc = apply_blocks_chunked(c, level, nblk, lams, 0, tau, 1, EPI_STORE, ap, (cudaStream_t)stream,
+                                    nullptr, nullptr))
+    return rc;
+  for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
+    const int nb = std::min(SPK_BMAX, nblk - b0);
+    SpkRowArgs a = row_args(c, level);
+    a.nblk = nb;
+    a.tau = tau;
+    a.final_step = final_step;
+    a.nan_flag = nan_flag;
+    for (int i = 0; i < nb; ++i) {
+      a.lam[i] = lams[b0 + i];
+      a.c1[i] = c1s[b0 + i];
+      a.c2[i] = c2s[b0 + i];
+    }
+    const long long off = (long long)b0 * n;
+    a.w = d_out + off; a.d = d_in + off; a.b = b + off; a.r = r + off; a.x = x + off; a.d_out = d_out + off;
+    cudaError_t e = spk_launch_cheb_rows(c->K, final_step ? 5 : 4, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cheb first update");
+  }
+  return SPK_OK;
+}
+
+int spk_cheb_split(spk_ctx* c, int level, int nblk) {
+  if (int rc = check_level(c, level)) return -rc;
+  return ((long long)nblk * c->dims[level].n >= SPK_SPLIT_CHEB_MIN) ? 1 : 0;
+}
+
 int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
                   const double* c2s, const double* d_in, double* r, double* x, double* d_out,
                   int final_step, int* nan_flag, void* stream) {

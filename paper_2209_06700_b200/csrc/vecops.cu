@@ -186,45 +186,69 @@ __global__ void __launch_bounds__(256) transfer_cols_kernel(const __grid_constan
   *dst = val;
 }
 
-// ---- row-parallel Chebyshev kernels: op 0 start (r = b, x = 0, d = Dinv r / theta),
-//      op 1 update after w = A d (r -= w; x += d; d = c1 d + c2 Dinv r), op 2 = op 1 fused with the
-//      final "return x + d" (multigrid.py:82-88) + NaN flag. The Jacobi diagonal is recomputed from the
-//      node class (row-uniform x/y factors, per-node z factor); no index divisions per node.
+// ---- pointwise Chebyshev kernels over the owned nodes [row0*nz, (row0+nrows)*nz) of a level:
+//      op 0 start (r = b, x = 0, d = Dinv r / theta), op 1 update after w = A d (r -= w; x += d;
+//      d = c1 d + c2 Dinv r), op 2 = op 1 fused with the final "return x + d" (multigrid.py:82-88)
+//      + NaN flag. Dinv comes from a per-CTA table over the (K+1)^3 node classes x blocks (no
+//      per-node division); flat node ranges keep every lane busy (rows of 2^l k + 1 nodes).
+template <int K>
+__device__ __forceinline__ int node_class(int i, int n, int E) {
+  if (E == 0) return 0;
+  const int r = i % K;
+  if (r != 0) return r;
+  return (i == 0 || i == n - 1) ? K : 0;
+}
+
 template <int K, int OP>
-__global__ void __launch_bounds__(128) cheb_rows_kernel(const __grid_constant__ SpkRowArgs a) {
+__global__ void __launch_bounds__(256) cheb_rows_kernel(const __grid_constant__ SpkRowArgs a) {
+  constexpr int K1 = K + 1, NCLS = K1 * K1 * K1;
+  __shared__ double inv_tab[NCLS * SPK_BMAX];
   const SpkDims& g = a.g;
-  const int rpc = blockDim.x / a.tpr;  // rows per CTA
-  const int row = a.row0 + blockIdx.x * rpc + threadIdx.x / a.tpr;
-  if (row >= a.row0 + a.nrows) return;
-  const int x = row / g.ny, y = row - x * g.ny;
-  double mx, kx, my, ky;
-  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], x + g.x0, g.Exg, mx, kx);
-  dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], y, g.Ey, my, ky);
-  const bool bxy = a.constrained && ((g.Ex > 0 && (x + g.x0 <= 0 || x + g.x0 >= g.nxg - 1)) ||
-                                     (g.Ey > 0 && (y == 0 || y == g.ny - 1)));
-  const long long base = (long long)row * g.nz;
-  bool bad = false;
-  for (int z = threadIdx.x % a.tpr; z < g.nz; z += a.tpr) {
-    const bool bnd = bxy || (a.constrained && g.Ez > 0 && (z == 0 || z == g.nz - 1));
-    double mz, kz;
-    dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], z, g.Ez, mz, kz);
+  // class table: node class (cx, cy, cz) -> 1 / (lam_b dm + tau dk), using one representative node
+  for (int e = threadIdx.x; e < NCLS * a.nblk; e += blockDim.x) {
+    const int b = e / NCLS, c = e - b * NCLS;
+    const int cx = c / (K1 * K1), cy = (c / K1) % K1, cz = c % K1;
+    auto rep = [&](int cls, int E) { return cls == K ? 0 : (cls == 0 ? K : cls); };  // a node of that class
+    double mx, kx, my, ky, mz, kz;
+    dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], rep(cx, g.Exg), g.Exg, mx, kx);
+    dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], rep(cy, g.Ey), g.Ey, my, ky);
+    dk_diag1<K>(&a.t.Me[0][0], &a.t.Ke[0][0], rep(cz, g.Ez), g.Ez, mz, kz);
     const double dm = (mx * my) * mz;
     const double dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
-    const long long i0 = base + z;
+    inv_tab[e] = 1.0 / (a.lam[b] * dm + a.tau * dk);
+  }
+  __syncthreads();
+  const unsigned plane = (unsigned)g.ny * (unsigned)g.nz;
+  const unsigned n0 = (unsigned)a.row0 * (unsigned)g.nz;
+  const unsigned n1 = n0 + (unsigned)a.nrows * (unsigned)g.nz;
+  bool bad = false;
+  for (unsigned i0 = n0 + blockIdx.x * blockDim.x + threadIdx.x; i0 < n1; i0 += gridDim.x * blockDim.x) {
+    const unsigned x = i0 / plane, rem = i0 - x * plane;
+    const unsigned y = rem / (unsigned)g.nz, z = rem - y * (unsigned)g.nz;
+    const int xg = (int)x + g.x0;
+    const bool bnd = a.constrained && ((g.Ex > 0 && (xg <= 0 || xg >= g.nxg - 1)) ||
+                                       (g.Ey > 0 && (y == 0 || (int)y == g.ny - 1)) ||
+                                       (g.Ez > 0 && (z == 0 || (int)z == g.nz - 1)));
+    const int cls = bnd ? 0 : (node_class<K>(xg, g.nxg, g.Exg) * K1 + node_class<K>((int)y, g.ny, g.Ey)) * K1 +
+                                  node_class<K>((int)z, g.nz, g.Ez);
     for (int b = 0; b < a.nblk; ++b) {
       const long long i = (long long)b * g.n + i0;
-      const double inv = bnd ? 1.0 : 1.0 / (a.lam[b] * dm + a.tau * dk);
+      const double inv = bnd ? 1.0 : inv_tab[b * NCLS + cls];
       if constexpr (OP == 0) {
         const double r = a.b[i];
         a.r[i] = r;
         a.x[i] = 0.0;
         a.d_out[i] = (inv * r) / a.c1[b];
+      } else if constexpr (OP == 3) {  // start from x = 0 without materialising r = b, x = 0
+        a.d_out[i] = (inv * a.b[i]) / a.c1[b];
       } else {
+        // OP 1/2: general update; OP 4/5: first update after OP 3 (r = b, x = 0 implicit)
+        constexpr bool FIRST = (OP >= 4);
         const double dq = a.d[i];
-        const double rn = a.r[i] - a.w[i];
-        const double xq = a.x[i] + dq;
+        const double rn = (FIRST ? a.b[i] : a.r[i]) - a.w[i];
+        const double xq = FIRST ? dq : a.x[i] + dq;
         const double dn = a.c1[b] * dq + a.c2[b] * (inv * rn);
-        if constexpr (OP == 1) {
+        if constexpr (OP == 1 || OP == 4) {
           a.r[i] = rn;
           a.x[i] = xq;
           a.d_out[i] = dn;
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(128) cheb_rows_kernel(const __grid_constant__ 
       }
     }
   }
-  if (OP == 2 && bad && a.nan_flag) atomicOr(a.nan_flag, 1);
+  if ((OP == 2 || OP == 5) && bad && a.nan_flag) atomicOr(a.nan_flag, 1);
 }
 
 // ---- (D (x) I) u : out_i = sum_j D_ij in_j (pointwise, all stages in registers) ----
@@ -584,14 +608,19 @@ cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s)
 }
 
 cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s) {
-  const int rpc = 128 / a.tpr;
-  const int nb = (a.nrows + rpc - 1) / rpc;
-  if (nb <= 0) return cudaSuccess;
+  const long long nodes = (long long)a.nrows * a.g.nz;
+  if (nodes <= 0) return cudaSuccess;
+  long long nbl = (nodes + 255) / 256;
+  if (nbl > 148LL * 8) nbl = 148LL * 8;
+  const int nb = (int)nbl;
 #define SPK_ROWS(KK)                                                                   \
   switch (op) {                                                                        \
-    case 0: cheb_rows_kernel<KK, 0><<<nb, 128, 0, s>>>(a); break;                     \
-    case 1: cheb_rows_kernel<KK, 1><<<nb, 128, 0, s>>>(a); break;                     \
-    default: cheb_rows_kernel<KK, 2><<<nb, 128, 0, s>>>(a); break;                    \
+    case 0: cheb_rows_kernel<KK, 0><<<nb, 256, 0, s>>>(a); break;                     \
+    case 1: cheb_rows_kernel<KK, 1><<<nb, 256, 0, s>>>(a); break;                     \
+    case 2: cheb_rows_kernel<KK, 2><<<nb, 256, 0, s>>>(a); break;                     \
+    case 3: cheb_rows_kernel<KK, 3><<<nb, 256, 0, s>>>(a); break;                     \
+    case 4: cheb_rows_kernel<KK, 4><<<nb, 256, 0, s>>>(a); break;                     \
+    default: cheb_rows_kernel<KK, 5><<<nb, 256, 0, s>>>(a); break;                    \
   }
   switch (K) {
     case 1: SPK_ROWS(1) break;

@@ -175,6 +175,19 @@ class _DeviceVCycle:
         else:
             lams = _lib.dbl_array(self._block_lams())
             nb = self.nrows
+            deg = self.config.smoother_degree
+            if zero_start and deg >= 2 and _lib.load().spk_cheb_split(h.ctx, level, nb) == 1:
+                # large level: d = Dinv b / theta, then the first step with r = b, x = 0 implicit
+                _lib.call("spk_cheb_start", h.ctx, level, nb, lams, self.tau, thetas, ptr(b), ptr(lv.d), st)
+                coefs = [sm.coefficients() for sm in sms]
+                self._halo(level, lv.d)
+                _lib.call("spk_cheb_first_step", h.ctx, level, nb, lams, self.tau,
+                          _lib.dbl_array([c[0][0] for c in coefs]), _lib.dbl_array([c[0][1] for c in coefs]),
+                          ptr(b), ptr(lv.d), ptr(lv.r), ptr(lv.x), ptr(lv.d2), 1 if deg == 2 else 0,
+                          ptr(self._flags[level:]), st)
+                lv.d, lv.d2 = lv.d2, lv.d
+                self._cheb_steps(level, lv, coefs, first=1)
+                return
             if zero_start:
                 _lib.call("spk_cheb_init", h.ctx, level, nb, lams, self.tau, thetas, ptr(b), ptr(lv.r), ptr(lv.x),
                           ptr(lv.d), st)
@@ -187,8 +200,15 @@ class _DeviceVCycle:
         if deg == 1:
             _lib.call("spk_axpy_flag", lv.x.numel(), ptr(lv.x), ptr(lv.d), flag, st)
             return
-        coefs = [sm.coefficients() for sm in sms]
-        for k in range(deg - 1):
+        self._cheb_steps(level, lv, [sm.coefficients() for sm in sms], first=0)
+
+    def _cheb_steps(self, level, lv, coefs, first):
+        """Chebyshev steps first .. deg-2 (the last one fused with "return x + d")."""
+        h = self.hierarchy
+        st = stream_ptr(h.device)
+        deg = self.config.smoother_degree
+        flag = ptr(self._flags[level:])
+        for k in range(first, deg - 1):
             final = 1 if k == deg - 2 else 0  # last step also performs "return x + d" (fused)
             self._halo(level, lv.d)
             if self.pair:
