@@ -134,6 +134,8 @@ int spk_cheb_start(spk_ctx* ctx, int level, int nblk, const double* lams, double
 int spk_cheb_first_step(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* c1s,
                         const double* c2s, const double* b, const double* d_in, double* r, double* x,
                         double* d_out, int final_step, int* nan_flag, void* stream);
+/* Chebyshev steps of levels with at least min_block_dofs (blocks x DoFs) run split (default 2^20) */
+int spk_set_cheb_split(spk_ctx* ctx, long long min_block_dofs);
 /* 1 if the Chebyshev steps of this level run split (K1 STORE + pointwise update), 0 if fused */
 int spk_cheb_split(spk_ctx* ctx, int level, int nblk);
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,

@@ -21,6 +21,7 @@ struct spk_ctx {
   double xi[SPK_KMAX + 1];
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
   int target_ctas = 0;    // 0: automatic x-chunking
+  long long split_cheb_min = 1LL << 20;  // block-DoFs from which Chebyshev steps run split
   // device scratch (lazily allocated on first device call)
   double* partial = nullptr;
   unsigned* counter = nullptr;
@@ -242,9 +243,8 @@ SpkRowArgs row_args(const spk_ctx* c, int level) {
 }
 
 // the fused K1 Chebyshev epilogue is latency-bound on its global operands at large levels: there
-// the step runs as a K1 STORE of w = A d followed by the row-parallel update (more bytes, near the
-// HBM roofline); small (L2-resident) levels keep the single fused launch
-constexpr long long SPK_SPLIT_CHEB_MIN = 1LL << 20;
+// the step runs as a K1 STORE of w = A d followed by the pointwise update (more bytes, near the
+// HBM roofline); small (L2-resident) levels keep the single fused launch (ctx->split_cheb_min)
 
 }  // namespace
 
@@ -405,6 +405,12 @@ int spk_set_chunks(spk_ctx* c, int target_ctas) {
   return SPK_OK;
 }
 
+int spk_set_cheb_split(spk_ctx* c, long long min_block_dofs) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  c->split_cheb_min = min_block_dofs;
+  return SPK_OK;
+}
+
 int spk_stage_apply(spk_ctx* c, int level, int Q, const double* DM, const double* DK, int constrained,
                     const double* u, long long su, double* v, long long sv, void* stream) {
   if (int rc = check_level(c, level)) return rc;
@@ -548,7 +554,7 @@ int spk_cheb_first_step(spk_ctx* c, int level, int nblk, const double* lams, dou
 
 int spk_cheb_split(spk_ctx* c, int level, int nblk) {
   if (int rc = check_level(c, level)) return -rc;
-  return ((long long)nblk * c->dims[level].n >= SPK_SPLIT_CHEB_MIN) ? 1 : 0;
+  return ((long long)nblk * c->dims[level].n >= c->split_cheb_min) ? 1 : 0;
 }
 
 int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
@@ -556,7 +562,7 @@ int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double ta
                   int final_step, int* nan_flag, void* stream) {
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
-  if ((long long)nblk * n >= SPK_SPLIT_CHEB_MIN) {
+  if ((long long)nblk * n >= c->split_cheb_min) {
     // w = A d into d_out (constrained: boundary rows carry d), then the pointwise update
     SpkApplyArgs ap = base_args(c, level);
     ap.u = d_in; ap.su = n; ap.v = d_out; ap.sv = n;

@@ -113,7 +113,8 @@ def test_slab_operators_and_transfers(cuda, k, L, world):
 
 
 # ---------------------------------------------------------------------------------------------
-def _vcycle_worker(rank, world, k, L, deg):
+def _vcycle_worker(rank, world, k, L, deg, split=1 << 62):
+    from paper_2209_06700_b200 import _lib
     from paper_2209_06700_b200.fem import build_hierarchy
     from paper_2209_06700_b200.multigrid import MultiBlockSolver, VCycleConfig
     from paper_2209_06700_b200.slab import DistMultiBlockSolver, SlabHierarchy, SlabPartition
@@ -122,6 +123,7 @@ def _vcycle_worker(rank, world, k, L, deg):
     lams = [3.2, 2.1]
     part = SlabPartition(k, L, world, rank)
     sh = SlabHierarchy(L, k, part, device="cuda:0")
+    _lib.call("spk_set_cheb_split", sh.ctx, split)  # 0: split Chebyshev steps on the slab windows
     full = build_hierarchy(3, L, k, device="cuda:0")
     ref = MultiBlockSolver(full, lams, 1e-2, cfg)
     dsv = DistMultiBlockSolver(sh, lams, 1e-2, cfg)
@@ -134,9 +136,10 @@ def _vcycle_worker(rank, world, k, L, deg):
     return lam_err, float((xg - x_ref).abs().max() / x_ref.abs().max()), part.counters.halo_exchanges
 
 
-@pytest.mark.parametrize("k,L,world,deg", [(2, 4, 2, 3), (1, 4, 4, 5), (4, 3, 2, 2)])
-def test_distributed_vcycle_matches_whole_mesh(cuda, k, L, world, deg):
-    res = _run(_vcycle_worker, world, k, L, deg)
+@pytest.mark.parametrize("k,L,world,deg,split", [(2, 4, 2, 3, 1 << 62), (1, 4, 4, 5, 1 << 62), (4, 3, 2, 2, 1 << 62),
+                                                 (2, 4, 2, 3, 0), (3, 3, 2, 5, 0)])
+def test_distributed_vcycle_matches_whole_mesh(cuda, k, L, world, deg, split):
+    res = _run(_vcycle_worker, world, k, L, deg, split)
     for r, (lam_err, err, nex) in res.items():
         assert lam_err < 1e-12, (r, lam_err)
         assert err < 1e-12, (r, err)

@@ -264,3 +264,23 @@ def test_perfmodel_counters_on_device_steps(cuda):
     v = validate_against_counters(reps, 4)
     assert v.ok, v.mismatches
     assert v.predicted_speedup == 4
+
+
+@pytest.mark.parametrize("dim,k,L,nblk", [(3, 2, 3, 3), (3, 4, 2, 1), (2, 3, 3, 2), (1, 2, 4, 4), (3, 1, 4, 2)])
+@pytest.mark.parametrize("split", [0, 1 << 62])
+def test_vcycle_split_and_fused_chebyshev_match_oracle(cuda, dim, k, L, nblk, split):
+    """Large levels run each Chebyshev step as K1 STORE + pointwise update (zero start without
+    materialising r = b, x = 0); small ones keep the fused K1 epilogue. Force each path on every
+    level and check both against the oracle (degrees 1, 2, 3, 5: the first / final-step variants)."""
+    from paper_2209_06700_b200 import _lib
+
+    h, o = build_hierarchy(dim, L, k), Hierarchy(dim, L, k)
+    _lib.call("spk_set_cheb_split", h.ctx, split)
+    rng = np.random.default_rng(21)
+    lams = [1.7, 3.1, 0.6, 8.0][:nblk]
+    b = np.where(o.finest.interior_mask, rng.standard_normal((nblk, o.n)), 0.0)
+    for deg in (1, 2, 3, 5):
+        cfg = VCycleConfig(smoother_degree=deg)
+        dev = MultiBlockSolver(h, lams, 0.03, cfg)
+        ref = OS.VCycle(o, lams, 0.03, OS.Config(smoother_degree=deg))
+        assert rel(dev.apply(b), ref.apply(b)) < 1e-11, (deg, split)
