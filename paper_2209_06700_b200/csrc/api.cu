@@ -135,10 +135,10 @@ int ensure_scratch(spk_ctx* c, int need) {
 }
 
 // x-chunking of the sliding window: enough CTAs to fill every SM about twice
-void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb) {
-  static const int TYE[5] = {0, 16, 8, 5, 4}, TZE[5] = {0, 16, 8, 5, 4};  // = Tile<K> (stage_apply.cuh)
-  const int gz = (a.g.Ez + 1 + TZE[K] - 1) / TZE[K];
-  const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + TYE[K] - 1) / TYE[K];
+void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb, int Qcta) {
+  const int tye = spk_apply_geo(K, Qcta, 2), tze = spk_apply_geo(K, Qcta, 3);  // the kernel's (y,z) tile
+  const int gz = (a.g.Ez + 1 + tze - 1) / tze;
+  const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + tye - 1) / tye;
   const long long tiles = (long long)gz * gy * nb;
   if (a.g.Ex == 0) { a.nchunks = 1; a.xe_chunk = 1; a.ex_begin = 0; a.ex_end = 0; return; }
   if (a.ex_end <= a.ex_begin) { a.ex_begin = 0; a.ex_end = a.g.Ex; }
@@ -180,6 +180,7 @@ int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a0, 
       a.DK[i][j] *= a0.hk;
     }
   a.dm_identity = ident ? 1 : 0;  // D_M diagonal (e.g. I (x) M): Q fewer FMAs per stage-DoF
+  set_chunking(c, a, c->K, block_mode ? a.nblk / Q : 1, Q);
   for (int i = 0; i < SPK_BMAX; ++i) a.lam[i] *= a0.hd;
   a.tau *= a0.hk;
   a.jre *= a0.hd;
@@ -213,7 +214,6 @@ int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, in
       a.c1[i] = c1s ? c1s[b0 + i] : 0.0;
       a.c2[i] = c2s ? c2s[b0 + i] : 0.0;
     }
-    set_chunking(c, a, c->K, nb / per_cta);
     // blocks are addressed as blk*su from the base pointer, so pass the unshifted base
     int rc = launch_apply(c, per_cta, true, epi, a, s);
     if (rc) return rc;
@@ -424,7 +424,6 @@ int spk_stage_apply(spk_ctx* c, int level, int Q, const double* DM, const double
       a.DM[i][j] = DM[i * Q + j];
       a.DK[i][j] = DK[i * Q + j];
     }
-  set_chunking(c, a, c->K, 1);
   return launch_apply(c, Q, false, EPI_STORE, a, (cudaStream_t)stream);
 }
 
@@ -448,7 +447,6 @@ int spk_stage_apply_slab(spk_ctx* c, int level, int Q, const double* DM, const d
       a.DM[i][j] = DM[i * Q + j];
       a.DK[i][j] = DK[i * Q + j];
     }
-  set_chunking(c, a, c->K, 1);
   return launch_apply(c, Q, false, EPI_STORE, a, (cudaStream_t)stream);
 }
 
@@ -472,7 +470,6 @@ int spk_pair_apply(spk_ctx* c, int level, double re, double im, double tau, int 
   a.constrained = constrained;
   a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
   a.DK[0][0] = tau; a.DK[1][1] = tau;
-  set_chunking(c, a, c->K, 1);
   return launch_apply(c, 2, false, EPI_STORE, a, (cudaStream_t)stream);
 }
 
@@ -605,7 +602,6 @@ int spk_pair_residual(spk_ctx* c, int level, double re, double im, double tau, c
   a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
   a.DK[0][0] = tau; a.DK[1][1] = tau;
   a.tau = tau; a.jre = re; a.jim = im; a.c2[0] = c2;
-  set_chunking(c, a, c->K, 1);
   return launch_apply(c, 2, false, EPI_RESID, a, (cudaStream_t)stream);
 }
 
@@ -636,7 +632,6 @@ int spk_pair_cheb_step(spk_ctx* c, int level, double re, double im, double tau, 
   a.DM[0][0] = re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = re;
   a.DK[0][0] = tau; a.DK[1][1] = tau;
   a.tau = tau; a.jre = re; a.jim = im; a.c1[0] = c1; a.c2[0] = c2;
-  set_chunking(c, a, c->K, 1);
   return launch_apply(c, 2, false, EPI_CHEB, a, (cudaStream_t)stream);
 }
 
@@ -655,14 +650,12 @@ int spk_dinv_norm(spk_ctx* c, int level, int pair, double lam_or_re, double im, 
   int rc;
   if (!pair) {
     a.nblk = 1; a.blk_base = 0; a.lam_uniform = 1; a.lam[0] = lam_or_re;
-    set_chunking(c, a, c->K, 1);
-    rc = launch_apply(c, 1, true, EPI_DINV, a, (cudaStream_t)stream, &nctas);
+      rc = launch_apply(c, 1, true, EPI_DINV, a, (cudaStream_t)stream, &nctas);
   } else {
     a.DM[0][0] = lam_or_re; a.DM[0][1] = -im; a.DM[1][0] = im; a.DM[1][1] = lam_or_re;
     a.DK[0][0] = tau; a.DK[1][1] = tau;
     a.jre = lam_or_re; a.jim = im;
-    set_chunking(c, a, c->K, 1);
-    rc = launch_apply(c, 2, false, EPI_DINV, a, (cudaStream_t)stream, &nctas);
+      rc = launch_apply(c, 2, false, EPI_DINV, a, (cudaStream_t)stream, &nctas);
   }
   if (rc) return rc;
   if (nctas > c->partial_cap) return fail(SPK_ECUDA, "partial buffer too small");

@@ -105,3 +105,4 @@ cudaError_t spk_launch_update(long long n, int Q, const double* k, const double*
                               cudaStream_t s);
 cudaError_t spk_launch_mask(long long total, const SpkDims& g, double* u, double value, cudaStream_t s);
 int spk_apply_smem_bytes(int K, int Q);
+int spk_apply_geo(int K, int Q, int what);  // 0 smem bytes, 1 threads, 2 TYE, 3 TZE

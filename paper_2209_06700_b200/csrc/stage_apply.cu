@@ -22,7 +22,7 @@ cudaError_t spk_launch_apply(int K, int Q, bool block_mode, int epi, const SpkAp
   return cudaErrorInvalidValue;
 }
 
-static int geo(int K, int Q, int what) {
+int spk_apply_geo(int K, int Q, int what) {
   switch (K) {
     case 1: return spk_apply_geo_k1(Q, what);
     case 2: return spk_apply_geo_k2(Q, what);
@@ -32,5 +32,5 @@ static int geo(int K, int Q, int what) {
   return -1;
 }
 
-int spk_apply_smem_bytes(int K, int Q) { return geo(K, Q, 0); }
-int spk_apply_threads(int K, int Q) { return geo(K, Q, 1); }
+int spk_apply_smem_bytes(int K, int Q) { return spk_apply_geo(K, Q, 0); }
+int spk_apply_threads(int K, int Q) { return spk_apply_geo(K, Q, 1); }

@@ -38,8 +38,14 @@ template <> struct Tile<2> { static constexpr int TYE = 8, TZE = 8; };
 template <> struct Tile<3> { static constexpr int TYE = 5, TZE = 5; };
 template <> struct Tile<4> { static constexpr int TYE = 4, TZE = 4; };
 
+#ifndef SPK_Q1_TILE
+#define SPK_Q1_TILE 1
+#endif
 template <int K, int Q> struct Geo {
-  static constexpr int TYE = Tile<K>::TYE, TZE = Tile<K>::TZE;
+  // one stage / block per CTA leaves most threads idle in the Z / Y phases of a ~256-node tile:
+  // Q = 1 sweeps a SPK_Q1_TILE^2 larger tile (several X points per thread)
+  static constexpr int TSC = (Q == 1) ? SPK_Q1_TILE : 1;
+  static constexpr int TYE = Tile<K>::TYE * TSC, TZE = Tile<K>::TZE * TSC;
   static constexpr int TY = K * TYE, TZ = K * TZE;
   // 1 barrier per plane: Z, Y, X run on three plane buffers (see the pipeline below)
   static constexpr bool PIPE3 = true;

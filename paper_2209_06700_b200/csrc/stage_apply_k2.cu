@@ -9,7 +9,8 @@ cudaError_t spk_launch_apply_k2(int Q, bool block_mode, int epi, const SpkApplyA
 int spk_apply_geo_k2(int Q, int what) {
   switch (Q) {
 #define SPK_GEO(q) \
-  case q: return what == 0 ? (int)(sizeof(double) * Geo<2, q>::SMEM_DOUBLES) : Geo<2, q>::NT;
+  case q: return what == 0 ? (int)(sizeof(double) * Geo<2, q>::SMEM_DOUBLES) \
+               : what == 1 ? Geo<2, q>::NT : what == 2 ? Geo<2, q>::TYE : Geo<2, q>::TZE;
     SPK_GEO(1) SPK_GEO(2) SPK_GEO(3) SPK_GEO(4)
 #undef SPK_GEO
   }
