@@ -83,6 +83,7 @@ template <int K, int Q> struct Geo {
   // U load items
   static constexpr int LITEMS = Q * NYin * NZin;
   static constexpr int LIT = (LITEMS + NT - 1) / NT;
+  static_assert(LIT <= 32, "load items are flagged in one 32-bit mask");
   static constexpr int MINB = (NT == 256 && SMEM_DOUBLES * 8 <= 112 * 1024) ? 2 : 1;
 };
 
@@ -443,10 +444,12 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 
   // ---- fixed per-thread work descriptors ----
   const long long plane_stride = (long long)g.ny * g.nz;
-  // U-plane load items, fixed for the kernel: a 32-bit source offset (doubles from u), the shared
-  // address and a byte count (8, or 0 = zero-fill: slots outside the domain and, constrained,
-  // y/z-boundary nodes). One zero-filling 8-byte cp.async per item and plane, no branches.
-  unsigned loff[G::LIT], ldst[G::LIT], lnb[G::LIT];
+  // U-plane load items, fixed for the kernel: a 32-bit source byte offset (from u), the shared
+  // address, and one bit of `lzero` per item = zero-fill (slots outside the domain and, constrained,
+  // y/z-boundary nodes). One 8-byte cp.async per item and plane whose ignore-src predicate writes
+  // the zeros; no branches, no per-plane index math beyond one 64-bit add.
+  unsigned loff[G::LIT], ldst[G::LIT];
+  unsigned lzero = 0u;
   constexpr bool LTAIL = (G::LITEMS % NT) != 0;  // only the last item can be past the end
 #pragma unroll
   for (int i = 0; i < G::LIT; ++i) {
@@ -459,21 +462,25 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
     const bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
     const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
-    loff[i] = in ? static_cast<unsigned>(q * a.su + (long long)gy * g.nz + gz) : 0u;
-    lnb[i] = (in && !(a.constrained && bnd)) ? 8u : 0u;
+    loff[i] = in ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
+    if (!in || (a.constrained && bnd)) lzero |= 1u << i;
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
   auto load_plane = [&](int x, auto BUF) {
     const unsigned buf = parity_of(BUF);
-    const double* base = u + (long long)x * plane_stride;
+    const unsigned long long base =
+        reinterpret_cast<unsigned long long>(u) + (unsigned long long)x * (unsigned long long)plane_stride * 8ull;
     // constrained: the x-boundary planes are zero (uniform per plane)
     const bool xb = a.constrained && !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
+    const unsigned zmask = xb ? 0xFFFFFFFFu : lzero;
 #pragma unroll
     for (int i = 0; i < G::LIT; ++i) {
       if (LTAIL && i == G::LIT - 1 && tid + i * NT >= G::LITEMS) break;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ldst[i] + buf * UBUF),
-                   "l"(base + loff[i]), "r"(xb ? 0u : lnb[i]) : "memory");
+      asm volatile(
+          "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+          " cp.async.ca.shared.global [%0], [%1], 8, p;\n}\n" ::"r"(ldst[i] + buf * UBUF),
+          "l"(base + loff[i]), "r"(zmask & (1u << i)) : "memory");
     }
     cp_async_commit();
   };
@@ -822,8 +829,8 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
   const int gz = (a.g.Ez + 1 + G::TZE - 1) / G::TZE;
   const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + G::TYE - 1) / G::TYE;
   const int nb = BLOCK ? a.nblk / Q : 1;  // CTA groups of Q blocks
-  // the plane loads address a CTA's Q stage rows with 32-bit offsets from its first row
-  if ((long long)(Q - 1) * a.su + a.g.n > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
+  // the plane loads address a CTA's Q stage rows with 32-bit byte offsets from its first row
+  if (((long long)(Q - 1) * a.su + a.g.n) * 8 > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
   dim3 grid(gz, gy, a.nchunks * nb);
   if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
   kern<<<grid, G::NT, smem, s>>>(a);
