@@ -225,7 +225,7 @@ def run_ours(args):
     if world == 1:
         # public host-buffer entry point: chunked H2D / K1 / D2H overlap (pipeline.py)
         from paper_2209_06700_b200.pipeline import HostStageOperator
-        hop = HostStageOperator(hier, L, DM, DK)
+        hop = HostStageOperator(hier, L, DM, DK, chunks=4)  # steady-state optimum (tools/e2e_probe.py)
         hop.apply(u_host, v_host)
         torch.cuda.synchronize()
         e2.record(s)

@@ -5,7 +5,10 @@
 K1 window (spk_stage_apply_slab on the full level, elements [c*ce, (c+1)*ce)) runs on the compute
 stream once its planes (and the k-plane left halo from chunk c-1) have landed, and its output planes
 go back on a D2H stream. PCIe H2D and D2H run concurrently on separate copy engines, so the step
-costs about max(H2D, D2H) instead of their sum.
+costs about max(H2D, D2H) instead of their sum. The device buffers are double-buffered across calls:
+the inputs of call i+1 stream in while the outputs of call i stream out (call i+1's H2D only waits
+for the compute that last read its buffer set, two calls back). Every call still ends with the
+caller's stream waiting for its D2H, so v_host is complete once that stream is synchronised.
 """
 
 import numpy as np
@@ -31,8 +34,10 @@ class HostStageOperator:
         self.chunks = max(1, min(chunks, self.E))
         self.ce = (self.E + self.chunks - 1) // self.chunks
         dev = h.device
-        self.u = torch.empty((self.Q, self.n), dtype=torch.float64, device=dev)
-        self.v = torch.empty_like(self.u)
+        self.us = [torch.empty((self.Q, self.n), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.vs = [torch.empty_like(self.us[0]) for _ in range(2)]
+        self._parity = 0
+        self._cmp_done = [None, None]
         self.s_in = torch.cuda.Stream(dev)
         self.s_out = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.current_stream(dev)
@@ -57,7 +62,13 @@ class HostStageOperator:
         nchunks = (self.E + self.ce - 1) // self.ce
         ev_in = [torch.cuda.Event() for _ in range(nchunks)]
         ev_cmp = [torch.cuda.Event() for _ in range(nchunks)]
-        self.s_in.wait_stream(self.s_cmp)
+        par = self._parity
+        self._parity ^= 1
+        self.u, self.v = self.us[par], self.vs[par]
+        # the caller's prior work on its stream (e.g. filling u_host was host-side; device producers
+        # of this call's inputs are not involved) and the compute that last read this buffer set
+        if self._cmp_done[par] is not None:
+            self.s_in.wait_event(self._cmp_done[par])
         with torch.cuda.stream(self.s_in):
             for c in range(nchunks):
                 lo, hi = self._planes_in(c)
@@ -71,6 +82,9 @@ class HostStageOperator:
                       self.DK.ctypes.data_as(_lib.P_dbl), ptr(self.u), self.n, ptr(self.v), self.n, self.E, e0, e1,
                       1 if e1 == self.E else 0, self.s_cmp.cuda_stream)
             ev_cmp[c].record(self.s_cmp)
+        done = torch.cuda.Event()
+        done.record(self.s_cmp)
+        self._cmp_done[par] = done
         with torch.cuda.stream(self.s_out):
             for c in range(nchunks):
                 self.s_out.wait_event(ev_cmp[c])

@@ -25,3 +25,14 @@ for ch in (4, 8, 16, 32):
     op.apply(uh, vh); torch.cuda.synchronize()
     t = sorted(measure.event_time(lambda: op.apply(uh, vh)) for _ in range(5))[2]
     print(f"chunks={ch}: {t:.2f} ms/apply")
+# steady state: back-to-back applies (double-buffered device sets overlap call i's D2H with i+1's H2D)
+for ch in (4, 8, 16):
+    op = HostStageOperator(h, L, DM, DK, chunks=ch)
+    for _ in range(2):
+        op.apply(uh, vh)
+    torch.cuda.synchronize()
+    def loop():
+        for _ in range(10):
+            op.apply(uh, vh)
+    t = measure.event_time(loop) / 10
+    print(f"steady chunks={ch}: {t:.2f} ms/apply")
