@@ -1,6 +1,7 @@
 // C-ABI host layer of libspk: discretisation setup (Q_k element tables on GLL nodes, transfer
 // tables, per-level dims) and stream-ordered kernel launches. See include/spk.h for the contract.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -21,7 +22,10 @@ struct spk_ctx {
   double xi[SPK_KMAX + 1];
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
   int target_ctas = 0;    // 0: automatic x-chunking
-  long long split_cheb_min = 1LL << 20;  // block-DoFs from which Chebyshev steps run split
+  // block-DoFs from which Chebyshev steps run split; launches of >= 3 blocks always run split (their
+  // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
+  // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
+  long long split_cheb_min = 1LL << 18;
   // device scratch (lazily allocated on first device call)
   double* partial = nullptr;
   unsigned* counter = nullptr;
@@ -246,6 +250,10 @@ SpkRowArgs row_args(const spk_ctx* c, int level) {
 // the step runs as a K1 STORE of w = A d followed by the pointwise update (more bytes, near the
 // HBM roofline); small (L2-resident) levels keep the single fused launch (ctx->split_cheb_min)
 
+bool cheb_split(const spk_ctx* c, int level, int nblk) {
+  return nblk >= 3 || (long long)nblk * c->dims[level].n >= c->split_cheb_min;
+}
+
 }  // namespace
 
 extern "C" {
@@ -262,6 +270,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (max_level < 1 || max_level > 10)
     return fail(SPK_ECONFIG, "max_level must be in [1, 10], got " + std::to_string(max_level));
   spk_ctx* c = new spk_ctx();
+  if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -551,7 +560,7 @@ int spk_cheb_first_step(spk_ctx* c, int level, int nblk, const double* lams, dou
 
 int spk_cheb_split(spk_ctx* c, int level, int nblk) {
   if (int rc = check_level(c, level)) return -rc;
-  return ((long long)nblk * c->dims[level].n >= c->split_cheb_min) ? 1 : 0;
+  return cheb_split(c, level, nblk) ? 1 : 0;
 }
 
 int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
@@ -559,7 +568,7 @@ int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double ta
                   int final_step, int* nan_flag, void* stream) {
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
-  if ((long long)nblk * n >= c->split_cheb_min) {
+  if (cheb_split(c, level, nblk)) {
     // w = A d into d_out (constrained: boundary rows carry d), then the pointwise update
     SpkApplyArgs ap = base_args(c, level);
     ap.u = d_in; ap.su = n; ap.v = d_out; ap.sv = n;

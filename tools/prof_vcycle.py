@@ -12,6 +12,8 @@ from paper_2209_06700_b200.multigrid import MultiBlockSolver, VCycleConfig
 k = int(os.environ.get("K", 2)); L = int(os.environ.get("L", 7)); nb = int(os.environ.get("NB", 4))
 deg = int(os.environ.get("DEG", 3))
 h = build_hierarchy(3, L, k)
+if "SPLIT" in os.environ:  # Chebyshev split threshold (block-DoFs); 0 = always split
+    _lib.call("spk_set_cheb_split", h.ctx, int(os.environ["SPLIT"]))
 n = h.levels[L].n_dofs
 lams = [5.6, 2.9, 3.2, 16.0][:nb]
 tau = 1e-3
