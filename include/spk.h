@@ -134,6 +134,8 @@ int spk_cheb_start(spk_ctx* ctx, int level, int nblk, const double* lams, double
 int spk_cheb_first_step(spk_ctx* ctx, int level, int nblk, const double* lams, double tau, const double* c1s,
                         const double* c2s, const double* b, const double* d_in, double* r, double* x,
                         double* d_out, int final_step, int* nan_flag, void* stream);
+/* single-block K1 launches on whole-mesh 3D levels sweep 4 (or 2) x-ranges per CTA (default on) */
+int spk_set_vsplit(spk_ctx* ctx, int on);
 /* Chebyshev steps run split on levels with at least min_block_dofs (blocks x DoFs; default 2^18) and
  * always for >= 3 blocks (measured faster than the fused K1 epilogue there) */
 int spk_set_cheb_split(spk_ctx* ctx, long long min_block_dofs);

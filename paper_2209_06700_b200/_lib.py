@@ -54,6 +54,7 @@ _SIGS = {
                              c_vp, c_vp], c_int),
     "spk_cheb_split": ([c_vp, c_int, c_int], c_int),
     "spk_set_cheb_split": ([c_vp, c_ll], c_int),
+    "spk_set_vsplit": ([c_vp, c_int], c_int),
     "spk_pair_residual": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp], c_int),
     "spk_pair_cheb_init": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_pair_cheb_step": ([c_vp, c_int, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_int,

@@ -26,6 +26,7 @@ struct spk_ctx {
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
   long long split_cheb_min = 1LL << 18;
+  int vsplit = 1;         // single-block K1 launches sweep 4 x-ranges per CTA (virtual x-split)
   // device scratch (lazily allocated on first device call)
   double* partial = nullptr;
   unsigned* counter = nullptr;
@@ -197,6 +198,31 @@ int launch_apply(spk_ctx* c, int Q, bool block_mode, int epi, SpkApplyArgs& a0, 
 int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, int lam_uniform,
                          double tau, int constrained, int epi, SpkApplyArgs a, cudaStream_t s,
                          const double* c1s, const double* c2s) {
+  // one block: a CTA of Q = 1 leaves most threads idle in the Z / Y phases; sweep V consecutive
+  // x-ranges of the block as V "virtual blocks" instead (whole-mesh 3D levels with >= 8 elements)
+  const SpkDims& g = a.g;
+  // (not for the fused Chebyshev epilogue: its 4-stage variant spills at 128 registers)
+  if (nblk == 1 && c->vsplit && epi != EPI_CHEB && c->dim == 3 && g.Ex >= 8 && g.x0 == 0 && a.ex_begin == 0 &&
+      (a.ex_end == 0 || a.ex_end == g.Ex)) {
+    const int V = (g.Ex % 4 == 0) ? 4 : 2;
+    const int Ev = g.Ex / V;
+    const long long vs = (long long)c->K * Ev * g.ny * g.nz;
+    SpkApplyArgs b = a;
+    b.su = vs; b.sv = vs; b.se = vs;
+    b.vplanes = c->K * Ev;
+    b.g.Ex = Ev;
+    b.g.nx = c->K * Ev + 1;
+    b.g.n = (long long)b.g.nx * g.ny * g.nz;
+    b.ex_begin = 0; b.ex_end = Ev;
+    b.blk_base = 0; b.nblk = V;
+    b.lam_uniform = 1; b.lam[0] = lams[0];
+    b.tau = tau; b.constrained = constrained;
+    for (int i = 0; i < V; ++i) {
+      b.c1[i] = c1s ? c1s[0] : 0.0;
+      b.c2[i] = c2s ? c2s[0] : 0.0;
+    }
+    return launch_apply(c, V, true, epi, b, s);
+  }
   // launch in groups of at most SPK_BMAX blocks so per-block coefficients fit the parameter block;
   // inside a launch every CTA sweeps `per_cta` blocks together (1..4) to share the halo loads,
   // index math and barriers of the plane pipeline
@@ -271,6 +297,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
     return fail(SPK_ECONFIG, "max_level must be in [1, 10], got " + std::to_string(max_level));
   spk_ctx* c = new spk_ctx();
   if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
+  if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -411,6 +438,12 @@ int spk_apply_smem(int degree, int Q) { return spk_apply_smem_bytes(degree, Q); 
 int spk_set_chunks(spk_ctx* c, int target_ctas) {
   if (!c) return fail(SPK_ECONFIG, "null context");
   c->target_ctas = target_ctas;
+  return SPK_OK;
+}
+
+int spk_set_vsplit(spk_ctx* c, int on) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  c->vsplit = on;
   return SPK_OK;
 }
 

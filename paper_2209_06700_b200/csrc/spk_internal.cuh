@@ -45,6 +45,9 @@ struct SpkApplyArgs {
   int xe_chunk, nchunks;  // x-chunking of the sliding window
   int ex_begin, ex_end;   // element range in x whose nodes are produced (slab windows)
   int store_last;         // also produce the last vertex plane when ex_end == Ex
+  // virtual x-split (block mode): the CTA's Q "blocks" are Q consecutive x-ranges of ONE block,
+  // vplanes planes apart (su = sv = se = vplanes * plane); 0 = off
+  int vplanes;
   int constrained;
   int nblk;               // block mode: number of independent blocks
   int blk_base;           // block mode: index of the first block of this launch

@@ -270,38 +270,62 @@ __device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 
 template <int K, int Q, bool BLOCK, int EPI>
 __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q],
                                          const double* dtab, const double (&ith)[Q], int x, int y, int z,
-                                         long long gi, const double (&val)[Q], double& sumsq) {
-  // gi: node index of (x, y, z) in the level (x * ny*nz + y * nz + z), precomputed by the caller
+                                         long long gi, const double (&val)[Q], double& sumsq,
+                                         int qfirst = 0) {
+  // gi: node index of (x, y, z) in the level (x * ny*nz + y * nz + z), precomputed by the caller.
+  // Virtual x-split: stage q of the CTA sits q*vplanes planes further along x (its global x differs).
+  // Stages q < qfirst are skipped (the last vertex plane of a virtual range belongs to the next).
   const SpkDims& g = a.g;
   const long long ubase = (BLOCK ? (long long)b0 * a.su : 0) + gi;
   const long long ebase = (BLOCK ? (long long)b0 * a.se : 0) + gi;
   const long long vbase = (BLOCK ? (long long)b0 * a.sv : 0) + gi;
   const int slot0 = BLOCK ? b0 - a.blk_base : 0;
-  const bool bnd = a.constrained && on_boundary(g, x, y, z);
+  const bool vsplit = BLOCK && a.vplanes != 0;
+  const bool bnd_yz = a.constrained && ((g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+                                        (g.Ez > 0 && (z == 0 || z == g.nz - 1)));
+  bool bndq[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int xg = x + g.x0 + (vsplit ? q * a.vplanes : 0);
+    bndq[q] = bnd_yz || (a.constrained && g.Ex > 0 && (xg == 0 || xg == g.nxg - 1));
+  }
+  bool bnd = false;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) bnd |= bndq[q];
   double Av[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) Av[q] = val[q];
   if (bnd) {  // constrained boundary rows are the identity (rare: a real branch, not a select)
 #pragma unroll
-    for (int q = 0; q < Q; ++q) Av[q] = __ldg(a.u + ubase + q * a.su);
+    for (int q = 0; q < Q; ++q)
+      if (bndq[q]) Av[q] = __ldg(a.u + ubase + q * a.su);
   }
 
   if constexpr (EPI == EPI_STORE) {
     double* vp = a.v + vbase;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) __stcs(vp + q * a.sv, Av[q]);
+    for (int q = 0; q < Q; ++q)
+      if (q >= qfirst) __stcs(vp + q * a.sv, Av[q]);
   } else {
     // Jacobi diagonal (reference operator_diagonal fem.py:172-187, 1.0 on boundary): looked up in
     // the per-CTA table of node classes (no per-node division)
     constexpr int K1 = K + 1;
-    const int cls = (axis_class<K>(x + g.x0, g.nxg, g.Ex) * K1 + axis_class<K>(y, g.ny, g.Ey)) * K1 +
-                    axis_class<K>(z, g.nz, g.Ez);
+    const int cyz = axis_class<K>(y, g.ny, g.Ey) * K1 + axis_class<K>(z, g.nz, g.Ez);
+    const int cls = axis_class<K>(x + g.x0, g.nxg, g.Ex) * K1 * K1 + cyz;
     const double* dt = dtab + cls * Geo<K, Q>::DT_STRIDE;
     double z0[Q];  // Dinv applied to the quantity of the epilogue
     auto jacobi = [&](const double (&rr)[Q]) {
       if constexpr (BLOCK) {
+        if (vsplit) {  // per-stage x class (one block: table column 0)
 #pragma unroll
-        for (int q = 0; q < Q; ++q) z0[q] = (bnd ? 1.0 : dt[q]) * rr[q];
+          for (int q = 0; q < Q; ++q) {
+            const int cq = axis_class<K>(x + g.x0 + q * a.vplanes, g.nxg, g.Ex) * K1 * K1 + cyz;
+            z0[q] = (bndq[q] ? 1.0 : dtab[cq * Geo<K, Q>::DT_STRIDE]) * rr[q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) z0[q] = (bndq[q] ? 1.0 : dt[q]) * rr[q];
+        }
       } else {  // pair 2x2 block Jacobi (multigrid.py:268-276, 306-313)
         const double A_ = bnd ? 1.0 : dt[0], B_ = bnd ? 0.0 : dt[1];
         z0[0] = A_ * rr[0] + B_ * rr[1];
@@ -315,6 +339,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
       double* vp = a.v + vbase;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
+        if (q < qfirst) continue;
         vp[q * a.sv] = z0[q];
         sumsq = fma(z0[q], z0[q], sumsq);
       }
@@ -325,7 +350,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           rn[q] = __ldg(bp + q * a.se) - Av[q];
-          rp[q * a.se] = rn[q];
+          if (q >= qfirst) rp[q * a.se] = rn[q];
         }
       } else {  // EPI_CHEB:  x += d ; r -= A d ; d = c1 d + c2 Dinv r   (multigrid.py:82-87)
         const double* up = a.u + ubase;
@@ -335,8 +360,10 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
           rn[q] = rp[q * a.se] - Av[q];
           const double xq = xp[q * a.se] + dq[q];
           if (!a.final_step) {
-            rp[q * a.se] = rn[q];
-            xp[q * a.se] = xq;
+            if (q >= qfirst) {
+              rp[q * a.se] = rn[q];
+              xp[q * a.se] = xq;
+            }
           } else {
             xfin[q] = xq;
           }
@@ -354,14 +381,16 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
             dn = a.c1[slot] * dq[q] + a.c2[slot] * z0[q];
             if (a.final_step) {  // last step fused with "return x + d" (multigrid.py:88) + NaN check
               const double xn = xfin[q] + dn;
-              xp[q * a.se] = xn;
-              bad |= !isfinite(xn);
+              if (q >= qfirst) {
+                xp[q * a.se] = xn;
+                bad |= !isfinite(xn);
+              }
               continue;
             }
           } else {
             dn = z0[q] * ith[q];  // post-smoothing start: d = (Dinv r) / theta  (multigrid.py:77)
           }
-          dp[q * a.se] = dn;
+          if (q >= qfirst) dp[q * a.se] = dn;
         }
         if (bad && a.nan_flag) atomicOr(a.nan_flag, 1);
       }
@@ -435,9 +464,11 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   if (!xdeg) {
     ex0 = a.ex_begin + chunk * a.xe_chunk;
     ex1 = min(a.ex_end, ex0 + a.xe_chunk);
-    // first real element of the window (a first slab has padding planes x0 < 0 in front)
+    // first real element of the window (a first slab has padding planes x0 < 0 in front); with a
+    // virtual x-split every range starts one element early (the left neighbour range's last
+    // element, zero-filled for the first range)
     const int efirst = g.x0 < 0 ? -g.x0 / K : 0;
-    ecur = ex0 > efirst ? ex0 - 1 : ex0;
+    ecur = (ex0 > efirst || (BLOCK && a.vplanes)) ? ex0 - 1 : ex0;
     xs = K * ecur;
     nplanes = K * ex1 - xs + 1;
   }
@@ -450,6 +481,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   // the zeros; no branches, no per-plane index math beyond one 64-bit add.
   unsigned loff[G::LIT], ldst[G::LIT];
   unsigned lzero = 0u;
+  unsigned lq[Q];  // virtual x-split: items of stage q (their global x is q*vplanes further)
+#pragma unroll
+  for (int q = 0; q < Q; ++q) lq[q] = 0u;
   constexpr bool LTAIL = (G::LITEMS % NT) != 0;  // only the last item can be past the end
 #pragma unroll
   for (int i = 0; i < G::LIT; ++i) {
@@ -464,6 +498,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
     loff[i] = in ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
     if (!in || (a.constrained && bnd)) lzero |= 1u << i;
+#pragma unroll
+    for (int qq = 0; qq < Q; ++qq)
+      if (q == qq) lq[qq] |= 1u << i;
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
@@ -471,9 +508,19 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     const unsigned buf = parity_of(BUF);
     const unsigned long long base =
         reinterpret_cast<unsigned long long>(u) + (unsigned long long)x * (unsigned long long)plane_stride * 8ull;
-    // constrained: the x-boundary planes are zero (uniform per plane)
-    const bool xb = a.constrained && !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
-    const unsigned zmask = xb ? 0xFFFFFFFFu : lzero;
+    // constrained: the x-boundary planes are zero (uniform per plane); virtual x-split: per stage,
+    // and planes left of the domain (first range's halo element) are zero too
+    unsigned zmask = lzero;
+    if (BLOCK && a.vplanes) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int xg = x + g.x0 + q * a.vplanes;
+        if (xg < 0 || (a.constrained && (xg == 0 || xg == g.nxg - 1))) zmask |= lq[q];
+      }
+    } else {
+      const bool xb = a.constrained && !xdeg && (x + g.x0 == 0 || x + g.x0 == g.nxg - 1);
+      if (xb) zmask = 0xFFFFFFFFu;
+    }
 #pragma unroll
     for (int i = 0; i < G::LIT; ++i) {
       if (LTAIL && i == G::LIT - 1 && tid + i * NT >= G::LITEMS) break;
@@ -738,13 +785,17 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
           double val[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
+          // virtual x-split: only the last range owns it (the others' is the next range's plane 0)
           epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
-                                     (long long)(K * g.Ex) * plane_stride + pyz[j], val, sumsq);
+                                     (long long)(K * g.Ex) * plane_stride + pyz[j], val, sumsq,
+                                     (BLOCK && a.vplanes) ? Q - 1 : 0);
         }
         // carry the shared vertex and start the next element with this plane as its local 0
+        // (virtual x-split: the first range's halo element lies outside the domain -> no carry)
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const double carry = acc[j][q][K];
+          const bool ghost = BLOCK && a.vplanes && ecur + g.x0 / K + q * (a.vplanes / K) < 0;
+          const double carry = ghost ? 0.0 : acc[j][q][K];
 #pragma unroll
           for (int s = 0; s <= K; ++s) acc[j][q][s] = fma(cf.m(s, 0), pq[q], cf.s(s, 0) * qq[q]);
           acc[j][q][0] += carry;

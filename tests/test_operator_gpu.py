@@ -108,3 +108,29 @@ def test_full_size_separable_and_linear(cuda, k, L):
     lhs = float(torch.sum(y * ox))
     rhs = float(torch.sum(oty * x))
     assert abs(lhs - rhs) < 1e-11 * max(abs(lhs), 1.0)
+
+
+@pytest.mark.parametrize("k,L", [(1, 4), (2, 3), (3, 3), (4, 3), (2, 4)])
+def test_single_block_virtual_xsplit(cuda, k, L):
+    """One block runs as 4 x-ranges per CTA (virtual x-split): unconstrained / constrained applies,
+    the residual epilogue and a V-cycle agree with the oracle and with the plain Q = 1 launch."""
+    from paper_2209_06700_b200 import _lib
+    from paper_2209_06700_b200.multigrid import BlockSolver, VCycleConfig
+    from oracle import solvers as OS
+
+    h, o = build_hierarchy(3, L, k), Hierarchy(3, L, k)
+    rng = np.random.default_rng(31)
+    u = rng.standard_normal(o.n)
+    outs = {}
+    for on in (1, 0):
+        _lib.call("spk_set_vsplit", h.ctx, on)
+        ud = torch.from_numpy(u).cuda().reshape(1, -1)
+        outs[on] = (h.apply_block(L, 1.3, 0.07, ud).cpu().numpy()[0],
+                    h.apply_block(L, 1.3, 0.07, ud, constrained=True).cpu().numpy()[0],
+                    BlockSolver(h, 2.5, 0.03, VCycleConfig(smoother_degree=3)).apply(
+                        np.where(o.finest.interior_mask, u, 0.0)))
+    ref = (o.apply_shifted(L, 1.3, 0.07, u), o.apply_constrained(L, 1.3, 0.07, u),
+           OS.VCycle(o, [2.5], 0.03, OS.Config(smoother_degree=3)).apply(np.where(o.finest.interior_mask, u, 0.0)))
+    for a, b, r in zip(outs[1], outs[0], ref):
+        assert rel(a, r) < 1e-11
+        assert rel(a, b) < 1e-13
