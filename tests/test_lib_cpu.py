@@ -64,3 +64,31 @@ def test_hierarchy_guards():
         build_hierarchy(2, 8)
     with pytest.raises(ConfigurationError):
         build_hierarchy(2, 2, degree=5)
+
+
+def test_slab_window_host_side():
+    """spk_ctx_set_slab: validation and the local level sizes the Python slab layout relies on."""
+    from paper_2209_06700_b200.slab import SlabPartition
+
+    lib = _lib.load()
+    k, L, B = 2, 4, 4
+    ctx = _lib.c_vp()
+    assert lib.spk_ctx_create(3, L, k, _lib.ctypes.byref(ctx)) == 0
+    try:
+        for b in range(B):
+            part = SlabPartition(k, L, B, b)
+            for level in part.dist_levels:
+                w = part.window(level)
+                rc = lib.spk_ctx_set_slab(ctx, level, w.x_elems, w.x0, 2, w.x_elems, 1 if w.last else 0)
+                assert rc == 0, lib.spk_last_error()
+                npa, nd, hh, ne = _lib.c_int(), _lib.c_ll(), _lib.c_dbl(), _lib.c_int()
+                assert lib.spk_level_info(ctx, level, _lib.ctypes.byref(npa), _lib.ctypes.byref(nd),
+                                          _lib.ctypes.byref(hh), _lib.ctypes.byref(ne)) == 0
+                assert nd.value == w.local_numel and npa.value == w.nax
+        # invalid windows: elements past the mesh, misaligned offset, empty range
+        assert lib.spk_ctx_set_slab(ctx, L, 4, k * 14, 2, 4, 1) == 2
+        assert lib.spk_ctx_set_slab(ctx, L, 4, 1, 2, 4, 0) == 2
+        assert lib.spk_ctx_set_slab(ctx, L, 4, 0, 3, 3, 0) == 2
+        assert lib.spk_set_cheb_split(ctx, 0) == 0 and lib.spk_set_vsplit(ctx, 0) == 0
+    finally:
+        lib.spk_ctx_destroy(ctx)
