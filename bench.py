@@ -38,6 +38,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-step", action="store_true", help="skip the Radau IIA step timing (C3)")
     p.add_argument("--level", type=int, default=CFG["level"])
     return p.parse_args()
 
@@ -60,6 +61,35 @@ def config_dict(args, world, extra=None):
     if extra:
         d.update(extra)
     return d
+
+
+def radau_step_sample(steps=4):
+    """Time per Radau IIA step of C3 (BASELINE.json configs[2]: 32^3 Q2 hex, Q=3, tau=0.01, GMRES
+    rtol 1e-12, Chebyshev degree 3) on this GPU: the second half of the metric ("time per Radau IIA
+    step"). Device-resident state, CUDA events around `steps` steps after one warm-up step."""
+    import torch
+
+    from paper_2209_06700_b200.fem import build_hierarchy
+    from paper_2209_06700_b200.irk import StageSystem
+    from paper_2209_06700_b200.multigrid import VCycleConfig
+
+    tau = 0.01
+    ss = StageSystem(build_hierarchy(3, 5, 2), 3, tau, config=VCycleConfig(smoother_degree=3))
+    u = ss.initial_condition()
+    u, _ = ss.step(0.0, u)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = []
+    e0.record()
+    for i in range(steps):
+        u, rep = ss.step((i + 1) * tau, u)
+        its.append(rep.iterations)
+    e1.record()
+    torch.cuda.synchronize()
+    return {"config": "C3 (32^3 Q2 hex, Radau IIA Q=3, tau=0.01, rtol 1e-12, Chebyshev deg 3)",
+            "ms_per_step": e0.elapsed_time(e1) / steps, "steps": steps, "gmres_iterations": its,
+            "n_gpus": 1, "note": "per-config step times (C1, C3, C4, C5): tools/bench_steps.py, "
+                                 "profiles/r01_steps.jsonl"}
 
 
 def cpu_sample(Q, degree, tau, seconds=10.0):
@@ -255,6 +285,10 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu and world == 1:
         cpu = cpu_sample(Q, k, tau)
 
+    step = None
+    if rank == 0 and world == 1 and not args.no_step:
+        step = radau_step_sample()
+
     if rank == 0:
         launches_per_apply = 1 if op is None else op.launches_per_apply
         line = {"impl": "ours", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -270,7 +304,8 @@ def run_ours(args):
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(u_host.numel() * 8),
                         "d2h_bytes_per_step": int(v_host.numel() * 8), "ms_per_step": e2e_ms},
                 "gpu_launches": args.steps * launches_per_apply,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(),
+                "radau_step": step}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
