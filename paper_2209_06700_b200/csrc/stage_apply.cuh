@@ -866,9 +866,157 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   }
 }
 
+
+// ---- small levels: direct banded gather, one thread per node -------------------------------------
+// The sliding window pays its plane pipeline (cp.async latency + one barrier per plane) even when a
+// level has a few hundred nodes: ~20-30 us per launch on the coarse levels of every V-cycle. There a
+// thread per node gathers its (2K+1)^3 neighbourhood through L1 with the assembled 1D band rows (the
+// same reference-element tables and scaled shifts as K1) and runs K1's epilogue unchanged.
+#ifndef SPK_SMALL_WORK
+#define SPK_SMALL_WORK (1 << 23)   // n * (2K+1)^3 below which block-mode launches take this path
+#endif
+template <int K>
+struct Band {
+  // assembled 1D row of node class c (0 interior vertex, 1..K-1 element interior r, K first
+  // boundary vertex, K+1 last boundary vertex) at offset d in [-K, K]
+  static constexpr int NC = K + 2, W = 2 * K + 1;
+  __device__ static void build(double* m, double* k) {  // [NC][W] each
+    for (int idx = threadIdx.x; idx < NC * W; idx += blockDim.x) {
+      const int c = idx / W, d = idx % W - K;
+      double mv = 0.0, kv = 0.0;
+      auto add = [&](int i_loc, int j_loc) {
+        if (j_loc >= 0 && j_loc <= K) { mv += Hat<K>::M(i_loc, j_loc); kv += Hat<K>::S(i_loc, j_loc); }
+      };
+      if (c >= 1 && c < K) add(c, c + d);  // one element, local row c
+      else {
+        if (c != K) add(K, K + d);         // left element (absent at the first vertex)
+        if (c != K + 1) add(0, d);         // right element (absent at the last vertex)
+      }
+      m[idx] = mv;
+      k[idx] = kv;
+    }
+  }
+  __device__ static int cls(int i, int n) {
+    const int r = i % K;
+    if (r != 0) return r;
+    return i == 0 ? K : (i == n - 1 ? K + 1 : 0);
+  }
+};
+
+template <int K, int EPI>
+__global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
+  // one CTA row per block (blockIdx.y), one thread per node; the epilogue is K1's with Q = 1
+  using G = Geo<K, 1>;
+  using BD = Band<K>;
+  constexpr int W = BD::W;
+  __shared__ double dtab[G::DT_SZ];
+  __shared__ double bm[BD::NC * W], bk[BD::NC * W];
+  __shared__ double red[256];
+  const int tid = threadIdx.x;
+  const SpkDims g = a.g;
+  const int b0 = a.blk_base + (int)blockIdx.y;
+  double lamq[1], ith[1];
+  lamq[0] = a.lam_uniform ? a.lam[0] : a.lam[b0 - a.blk_base];
+  ith[0] = 1.0 / a.c2[b0 - a.blk_base];
+  if constexpr (EPI != EPI_STORE) {
+    constexpr int K1 = K + 1;
+    for (int idx = tid; idx < K1 * K1 * K1; idx += blockDim.x) {
+      const int cx = idx / (K1 * K1), cy = (idx / K1) % K1, cz = idx % K1;
+      double mx, kx, my, ky, mz, kz;
+      class_diag1<K>(cx, g.Ex, mx, kx);
+      class_diag1<K>(cy, g.Ey, my, ky);
+      class_diag1<K>(cz, g.Ez, mz, kz);
+      const double dm = (mx * my) * mz;
+      const double dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
+      dtab[idx * G::DT_STRIDE] = 1.0 / (lamq[0] * dm + a.tau * dk);
+    }
+  }
+  BD::build(bm, bk);
+  __syncthreads();
+  double sumsq = 0.0;
+  const long long i = (long long)blockIdx.x * blockDim.x + tid;
+  if (i < g.n) {
+    const int z = (int)(i % g.nz);
+    const long long t = i / g.nz;
+    const int y = (int)(t % g.ny), x = (int)(t / g.ny);
+    const int cm = a.constrained ? 1 : 0;
+    // per-axis band rows with out-of-range / masked (constrained boundary) neighbours zeroed, and
+    // clamped (always valid) neighbour indices: fixed trip counts, independent loads
+    double mzr[W], kzr[W], myr[W], kyr[W];
+    int zi[W], yi[W];
+    auto axis = [&](int c, int n, int E, double (&mr)[W], double (&kr)[W], int (&ix)[W]) {
+      const int cl = E == 0 ? 0 : BD::cls(c, n);
+#pragma unroll
+      for (int d = 0; d < W; ++d) {
+        const int j = c + d - K;
+        const bool ok = E == 0 ? (d == K) : (j >= cm && j <= n - 1 - cm);
+        mr[d] = ok ? (E == 0 ? 1.0 : bm[cl * W + d]) : 0.0;
+        kr[d] = ok ? (E == 0 ? 0.0 : bk[cl * W + d]) : 0.0;
+        ix[d] = min(max(j, 0), n - 1);
+      }
+    };
+    axis(z, g.nz, g.Ez, mzr, kzr, zi);
+    axis(y, g.ny, g.Ey, myr, kyr, yi);
+    const double* u = a.u + (long long)b0 * a.su;
+    double v = 0.0;
+    const int clx = g.Ex == 0 ? 0 : BD::cls(x, g.nx);
+    for (int dxi = 0; dxi < W; ++dxi) {
+      const int xx = x + dxi - K;
+      const bool okx = g.Ex == 0 ? (dxi == K) : (xx >= cm && xx <= g.nx - 1 - cm);
+      if (!okx) continue;
+      const double mxv = g.Ex == 0 ? 1.0 : bm[clx * W + dxi], kxv = g.Ex == 0 ? 0.0 : bk[clx * W + dxi];
+      if (mxv == 0.0 && kxv == 0.0) continue;
+      const double* plane = u + (long long)xx * g.ny * g.nz;
+      double A = 0.0, B = 0.0, C = 0.0;
+#pragma unroll
+      for (int dy = 0; dy < W; ++dy) {
+        const double* line = plane + (long long)yi[dy] * g.nz;
+        double uv[W];
+#pragma unroll
+        for (int dz = 0; dz < W; ++dz) uv[dz] = __ldg(line + zi[dz]);
+        double am = 0.0, ak = 0.0;
+#pragma unroll
+        for (int dz = 0; dz < W; ++dz) {
+          am = fma(mzr[dz], uv[dz], am);
+          ak = fma(kzr[dz], uv[dz], ak);
+        }
+        A = fma(myr[dy], am, A);
+        B = fma(kyr[dy], am, B);
+        C = fma(myr[dy], ak, C);
+      }
+      v = fma(mxv, fma(lamq[0], A, a.tau * (B + C)), v);
+      v = fma(a.tau * kxv, A, v);
+    }
+    double val[1] = {v};
+    epilogue<K, 1, true, EPI>(a, b0, lamq, dtab, ith, x, y, z, i, val, sumsq);
+  }
+  if constexpr (EPI == EPI_DINV) {
+    red[tid] = sumsq;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+      if (tid < off) red[tid] += red[tid + off];
+      __syncthreads();
+    }
+    if (tid == 0) a.partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = red[0];
+  }
+}
+
 template <int K, int Q, bool BLOCK, int EPI>
 cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
   using G = Geo<K, Q>;
+  constexpr long long W3 = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);
+  if constexpr (BLOCK) {
+    // small whole-mesh levels: direct gather kernel (no plane pipeline)
+    // (3D only: with a degenerate x axis the sliding window is a single plane and already cheap;
+    // k <= 3: at k = 4 the 729-point gather loses to the window, measured)
+    if (K <= 3 && a.vplanes == 0 && a.g.x0 == 0 && a.g.Ex > 0 && a.ex_begin == 0 && a.ex_end == a.g.Ex &&
+        a.store_last && a.g.n * W3 <= (long long)SPK_SMALL_WORK) {
+      dim3 grid((unsigned)((a.g.n + 255) / 256), (unsigned)a.nblk);
+      if (nctas_out) *nctas_out = (int)(grid.x * grid.y);
+      small_apply_kernel<K, EPI><<<grid, 256, 0, s>>>(a);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
   static bool configured = false;
   auto kern = stage_apply_kernel<K, Q, BLOCK, EPI>;
