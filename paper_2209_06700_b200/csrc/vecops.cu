@@ -139,23 +139,54 @@ __device__ __forceinline__ double transfer_value(const SpkTransferArgs& a, int i
   return val;
 }
 
-// sweep along the contiguous (z) axis: one CTA per input row, threads along the output row
+// sweep along the contiguous (z) axis: one warp per input row (8 rows per CTA), lanes along the
+// output row
 template <int K>
-__global__ void __launch_bounds__(128) transfer_rows_kernel(const __grid_constant__ SpkTransferArgs a) {
-  const long long o = blockIdx.x;
+__global__ void __launch_bounds__(256) transfer_rows_kernel(const __grid_constant__ SpkTransferArgs a) {
+  const long long o = (long long)blockIdx.x * 8 + threadIdx.y;
+  if (o >= a.outer) return;
   const double* src = a.in + o * (long long)a.nin - a.in_off;
   int x = 0, y = 0;
   if (a.mask) {  // final sweep of a 1D hierarchy: the row is (x, y) of the output level
     y = (int)(o % a.g.ny);
     x = (int)((o / a.g.ny) % a.g.nx);
   }
-  for (int il = a.o_begin + threadIdx.x; il < a.o_begin + a.nout; il += blockDim.x) {
+  for (int il = a.o_begin + threadIdx.x; il < a.o_begin + a.nout; il += 32) {
     double val = transfer_value<K>(a, il + a.out_off, src, 1);
     if (a.mask && bnd3(a.g, x, y, il)) val = 0.0;
     double* dst = a.out + o * (long long)a.onodes + il;
     if (a.accumulate) val += *dst;
     *dst = val;
   }
+}
+
+// strided sweep with a short inner extent (<= 256, e.g. the y sweep: inner = nz): CTA = by rows of
+// (outer row, output node) x bx lanes along the inner index, so no lane idles on a short row
+template <int K>
+__global__ void __launch_bounds__(256) transfer_cols_short_kernel(const __grid_constant__ SpkTransferArgs a) {
+  const long long row = (long long)blockIdx.x * blockDim.y + threadIdx.y;  // (o, il) flattened
+  const long long in_idx = threadIdx.x;
+  if (row >= a.outer * (long long)a.nout || in_idx >= a.inner) return;
+  const long long o = row / a.nout;
+  const int il = a.o_begin + (int)(row - o * a.nout);
+  const double* src = a.in + o * (long long)a.nin * a.inner + in_idx - (long long)a.in_off * a.inner;
+  double val = transfer_value<K>(a, il + a.out_off, src, a.inner);
+  if (a.mask) {
+    int x, y, z;
+    if (a.g.Ex > 0) {
+      x = il;
+      y = (int)(in_idx / a.g.nz);
+      z = (int)(in_idx - (long long)y * a.g.nz);
+    } else {
+      x = 0;
+      y = il;
+      z = (int)in_idx;
+    }
+    if (bnd3(a.g, x, y, z)) val = 0.0;
+  }
+  double* dst = a.out + (o * (long long)a.onodes + il) * a.inner + in_idx;
+  if (a.accumulate) val += *dst;
+  *dst = val;
 }
 
 // sweep along a strided axis (y: inner = nz, x: inner = ny*nz): grid (inner chunks, output node,
@@ -585,12 +616,25 @@ cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, in
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s) {
   if (a.nout <= 0 || a.outer <= 0) return cudaSuccess;
   if (a.inner == 1) {
-    const unsigned nb = (unsigned)a.outer;
+    const unsigned nb = (unsigned)((a.outer + 7) / 8);
+    const dim3 blk(32, 8);
     switch (K) {
-      case 1: transfer_rows_kernel<1><<<nb, 128, 0, s>>>(a); break;
-      case 2: transfer_rows_kernel<2><<<nb, 128, 0, s>>>(a); break;
-      case 3: transfer_rows_kernel<3><<<nb, 128, 0, s>>>(a); break;
-      case 4: transfer_rows_kernel<4><<<nb, 128, 0, s>>>(a); break;
+      case 1: transfer_rows_kernel<1><<<nb, blk, 0, s>>>(a); break;
+      case 2: transfer_rows_kernel<2><<<nb, blk, 0, s>>>(a); break;
+      case 3: transfer_rows_kernel<3><<<nb, blk, 0, s>>>(a); break;
+      case 4: transfer_rows_kernel<4><<<nb, blk, 0, s>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else if (a.inner <= 256) {
+    const int bx = (int)((a.inner + 31) / 32) * 32, by = 256 / bx;
+    const long long rows = a.outer * (long long)a.nout;
+    const unsigned nb = (unsigned)((rows + by - 1) / by);
+    const dim3 blk(bx, by);
+    switch (K) {
+      case 1: transfer_cols_short_kernel<1><<<nb, blk, 0, s>>>(a); break;
+      case 2: transfer_cols_short_kernel<2><<<nb, blk, 0, s>>>(a); break;
+      case 3: transfer_cols_short_kernel<3><<<nb, blk, 0, s>>>(a); break;
+      case 4: transfer_cols_short_kernel<4><<<nb, blk, 0, s>>>(a); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
