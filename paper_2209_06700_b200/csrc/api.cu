@@ -22,6 +22,7 @@ struct spk_ctx {
   double xi[SPK_KMAX + 1];
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
   int target_ctas = 0;    // 0: automatic x-chunking
+  int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   // block-DoFs from which Chebyshev steps run split; launches of >= 3 blocks always run split (their
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
@@ -139,6 +140,16 @@ int ensure_scratch(spk_ctx* c, int need) {
   return SPK_OK;
 }
 
+// whole-mesh 3D level that block-mode K1 launches run with the direct small-level kernel
+// (stage_apply.cuh launch_one: k <= 3 and n (2k+1)^3 <= SPK_SMALL_WORK)
+bool small_level(const spk_ctx* c, int level) {
+  const SpkDims& g = c->dims[level];
+  const long long w1 = 2LL * c->K + 1;
+  const bool whole = g.x0 == 0 && c->ex_begin[level] == 0 &&
+                     (c->ex_end[level] == 0 || c->ex_end[level] == g.Ex) && c->store_last[level];
+  return c->K <= 3 && c->dim == 3 && g.Ex > 0 && whole && g.n * w1 * w1 * w1 <= (long long)SPK_SMALL_WORK_HOST;
+}
+
 // x-chunking of the sliding window: enough CTAs to fill every SM about twice
 void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb, int Qcta) {
   const int tye = spk_apply_geo(K, Qcta, 2), tze = spk_apply_geo(K, Qcta, 3);  // the kernel's (y,z) tile
@@ -154,8 +165,17 @@ void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb, int Qcta) {
   long long nch = (target + tiles - 1) / tiles;
   if (nch < 1) nch = 1;
   if (nch > nel) nch = nel;
-  // keep at least 4 elements per chunk (the chunk pays one halo element)
+  // keep at least 4 elements per chunk (the chunk pays one halo element) ...
   while (nch > 1 && nel / nch < 4) --nch;
+  // ... unless that leaves part of the GPU idle: on small and mid-size levels a launch is bound by
+  // the plane-pipeline latency of one CTA, so shorter chunks (down to one element) that fill one wave
+  // of two CTAs per SM finish sooner than a few long ones
+  if (c->target_ctas <= 0 && c->fill_wave) {
+    const long long wave = 2LL * 148;
+    long long fill = wave / tiles;
+    if (fill > nel) fill = nel;
+    if (fill > nch) nch = fill;
+  }
   a.xe_chunk = (int)((nel + nch - 1) / nch);
   a.nchunks = (nel + a.xe_chunk - 1) / a.xe_chunk;
 }
@@ -202,8 +222,9 @@ int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, in
   // x-ranges of the block as V "virtual blocks" instead (whole-mesh 3D levels with >= 8 elements)
   const SpkDims& g = a.g;
   // (not for the fused Chebyshev epilogue: its 4-stage variant spills at 128 registers)
-  if (nblk == 1 && c->vsplit && epi != EPI_CHEB && c->dim == 3 && g.Ex >= 8 && g.x0 == 0 && a.ex_begin == 0 &&
-      (a.ex_end == 0 || a.ex_end == g.Ex)) {
+  // (not on levels the direct small-level kernel takes: stage_apply.cuh launch_one)
+  if (nblk == 1 && c->vsplit && !small_level(c, level) && epi != EPI_CHEB && c->dim == 3 && g.Ex >= 8 && g.x0 == 0 &&
+      a.ex_begin == 0 && (a.ex_end == 0 || a.ex_end == g.Ex)) {
     const int V = (g.Ex % 4 == 0) ? 4 : 2;
     const int Ev = g.Ex / V;
     const long long vs = (long long)c->K * Ev * g.ny * g.nz;
@@ -277,6 +298,9 @@ SpkRowArgs row_args(const spk_ctx* c, int level) {
 // HBM roofline); small (L2-resident) levels keep the single fused launch (ctx->split_cheb_min)
 
 bool cheb_split(const spk_ctx* c, int level, int nblk) {
+  // levels the direct small-level kernel takes (one CTA row per block) always fuse: there a launch
+  // costs more than the epilogue's loads
+  if (small_level(c, level)) return false;
   return nblk >= 3 || (long long)nblk * c->dims[level].n >= c->split_cheb_min;
 }
 
@@ -298,6 +322,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   spk_ctx* c = new spk_ctx();
   if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
   if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
+  if (const char* e = std::getenv("SPK_FILL_WAVE")) c->fill_wave = std::atoi(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;

@@ -12,6 +12,7 @@
 #define SPK_QMAX 4       // highest stage count of the fused stage-coupled kernel
 #define SPK_BMAX 16      // per-launch block-parameter slots (block mode)
 #define SPK_THREADS 256
+#define SPK_SMALL_WORK_HOST (1LL << 23)  // = SPK_SMALL_WORK (stage_apply.cuh): direct small-level kernel
 
 struct SpkDims {
   int nx, ny, nz;   // nodes per axis (1 for a degenerate axis)

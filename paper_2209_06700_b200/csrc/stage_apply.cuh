@@ -20,6 +20,7 @@
 // Every thread's work items are fixed for the whole kernel (no per-plane index arithmetic).
 // HBM traffic per apply: read u once (+ L2-resident halo), write v once = 16 B per stage-DoF.
 #pragma once
+#include <algorithm>
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
 
@@ -873,7 +874,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 // thread per node gathers its (2K+1)^3 neighbourhood through L1 with the assembled 1D band rows (the
 // same reference-element tables and scaled shifts as K1) and runs K1's epilogue unchanged.
 #ifndef SPK_SMALL_WORK
-#define SPK_SMALL_WORK (1 << 23)   // n * (2K+1)^3 below which block-mode launches take this path
+#define SPK_SMALL_WORK SPK_SMALL_WORK_HOST   // n * (2K+1)^3 below which block-mode launches take this path
 #endif
 template <int K>
 struct Band {
@@ -903,7 +904,10 @@ struct Band {
   }
 };
 
-template <int K, int EPI>
+// STAGED: the CTA first copies the x-planes its 256 nodes touch ([x_first - K, x_last + K]) into
+// shared memory with coalesced loads -- one memory latency -- and gathers from there (the direct
+// version waits out one L2 round trip per neighbour plane: 2K+1 of them)
+template <int K, int EPI, bool STAGED>
 __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
   // one CTA row per block (blockIdx.y), one thread per node; the epilogue is K1's with Q = 1
   using G = Geo<K, 1>;
@@ -912,9 +916,21 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
   __shared__ double dtab[G::DT_SZ];
   __shared__ double bm[BD::NC * W], bk[BD::NC * W];
   __shared__ double red[256];
+  extern __shared__ double ustage[];
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
   const int b0 = a.blk_base + (int)blockIdx.y;
+  const long long plane_n = (long long)g.ny * g.nz;
+  int p0 = 0;
+  if constexpr (STAGED) {
+    const long long i0 = (long long)blockIdx.x * blockDim.x;
+    const long long il = min(i0 + (long long)blockDim.x - 1, g.n - 1);
+    p0 = max((int)(i0 / plane_n) - K, 0);
+    const int p1 = min((int)(il / plane_n) + K, g.nx - 1);
+    const double* src = a.u + (long long)b0 * a.su + (long long)p0 * plane_n;
+    const long long cnt = (long long)(p1 - p0 + 1) * plane_n;
+    for (long long j = tid; j < cnt; j += blockDim.x) ustage[j] = __ldg(src + j);
+  }
   double lamq[1], ith[1];
   lamq[0] = a.lam_uniform ? a.lam[0] : a.lam[b0 - a.blk_base];
   ith[0] = 1.0 / a.c2[b0 - a.blk_base];
@@ -957,7 +973,7 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
     };
     axis(z, g.nz, g.Ez, mzr, kzr, zi);
     axis(y, g.ny, g.Ey, myr, kyr, yi);
-    const double* u = a.u + (long long)b0 * a.su;
+    const double* u = STAGED ? ustage - (long long)p0 * plane_n : a.u + (long long)b0 * a.su;
     double v = 0.0;
     const int clx = g.Ex == 0 ? 0 : BD::cls(x, g.nx);
     for (int dxi = 0; dxi < W; ++dxi) {
@@ -973,7 +989,7 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
         const double* line = plane + (long long)yi[dy] * g.nz;
         double uv[W];
 #pragma unroll
-        for (int dz = 0; dz < W; ++dz) uv[dz] = __ldg(line + zi[dz]);
+        for (int dz = 0; dz < W; ++dz) uv[dz] = STAGED ? line[zi[dz]] : __ldg(line + zi[dz]);
         double am = 0.0, ak = 0.0;
 #pragma unroll
         for (int dz = 0; dz < W; ++dz) {
@@ -1013,7 +1029,23 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
         a.store_last && a.g.n * W3 <= (long long)SPK_SMALL_WORK) {
       dim3 grid((unsigned)((a.g.n + 255) / 256), (unsigned)a.nblk);
       if (nctas_out) *nctas_out = (int)(grid.x * grid.y);
-      small_apply_kernel<K, EPI><<<grid, 256, 0, s>>>(a);
+      // staged x-planes: a run of 256 nodes touches at most 255/plane + 2 planes, plus K on each side
+      const long long plane = (long long)a.g.ny * a.g.nz;
+      const long long planes = std::min<long long>(a.g.nx, 255 / plane + 2 + 2 * K);
+      const size_t stage_bytes = (size_t)(planes * plane) * sizeof(double);
+      constexpr size_t STAGE_MAX = 160 * 1024;
+      if (stage_bytes <= STAGE_MAX) {
+        static bool configured_s = false;
+        if (!configured_s) {
+          cudaError_t e = cudaFuncSetAttribute(small_apply_kernel<K, EPI, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STAGE_MAX);
+          if (e != cudaSuccess) return e;
+          configured_s = true;
+        }
+        small_apply_kernel<K, EPI, true><<<grid, 256, stage_bytes, s>>>(a);
+      } else {
+        small_apply_kernel<K, EPI, false><<<grid, 256, 0, s>>>(a);
+      }
       return cudaGetLastError();
     }
   }
