@@ -97,7 +97,8 @@ class DirectComplexSystem(StageSystem):
                                                             constrained=True).reshape(v.shape)
                 pc = self._graphed(("real", bi), lambda v, vc=vc: vc.apply_device(v.reshape(1, -1),
                                                                                    check=False).reshape(v.shape))
-                zi, rep = gmres(op, pc, w[2 * bi].contiguous(), self.rel_tol, self.max_iter)
+                zi, rep = gmres(op, pc, w[2 * bi].contiguous(), self.rel_tol, self.max_iter,
+                                speculate=self.speculate)
                 z[2 * bi].copy_(zi)
             else:
                 op = lambda v, re=p.re, im=p.im: self._pair_op(re, im, v.contiguous())
@@ -105,7 +106,8 @@ class DirectComplexSystem(StageSystem):
                     pc = self._graphed(("presb", bi), lambda v, p=p, vc=vc: self._presb(p, vc, v))
                 else:
                     pc = self._graphed(("gmg", bi), lambda v, vc=vc: vc.apply_device(v.contiguous(), check=False))
-                zi, rep = gmres(op, pc, w[2 * bi : 2 * bi + 2].contiguous(), self.rel_tol, self.max_iter)
+                zi, rep = gmres(op, pc, w[2 * bi : 2 * bi + 2].contiguous(), self.rel_tol, self.max_iter,
+                                speculate=self.speculate)
                 z[2 * bi : 2 * bi + 2].copy_(zi)
             its.append(rep.iterations)
             if not rep.converged:

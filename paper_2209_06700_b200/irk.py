@@ -26,6 +26,10 @@ from .tableau import crout_lu, radau_iia, spectral_real
 from .tensor_ops import dense_combine
 
 
+# stage-DoFs below which a step is host-bound (GMRES with speculation; measured: C3 is, C5 / C4 are not)
+SPECULATE_MAX_DOFS = 1 << 22
+
+
 @dataclass
 class SolveReport:
     """Per-step record: outer GMRES iterations, V-cycles per stage (= its + 1), history."""
@@ -73,6 +77,9 @@ class StageSystem:
         self.vcycles = 0
         self.use_graphs = True
         self._graph = None
+        # host-bound small problems: overlap the host least squares with the next A P^{-1} product
+        # (krylov.gmres(speculate=True); costs one discarded application per solve)
+        self.speculate = self.Q * self.n <= SPECULATE_MAX_DOFS
 
     # ---- pieces ----
     def assemble_rhs(self, t_n, u_n):
@@ -123,7 +130,9 @@ class StageSystem:
         """u_{n+1} for device u_n (n,), and the SolveReport."""
         rhs = self.assemble_rhs(t_n, u_n)
         v0 = self.vcycles
-        k, rep = gmres(self.apply_system_operator, self.apply_preconditioner, rhs, self.rel_tol, self.max_iter)
+        k, rep = gmres(self.apply_system_operator, self.apply_preconditioner, rhs, self.rel_tol, self.max_iter,
+                       speculate=self.speculate)
+        self.vcycles -= rep.speculative_applies
         if check:
             self.precond.check_finite()
         u_next = u_n.clone()

@@ -34,6 +34,7 @@ class KrylovReport:
     residual_history: list = field(default_factory=list)
     converged: bool = False
     reduction_achieved: float = 1.0
+    speculative_applies: int = 0   # discarded A P^{-1} applications (gmres(speculate=True))
 
 
 _NULL_CTX = None
@@ -139,11 +140,17 @@ class _Ops:
             torch.div(w, h, out=out)
 
 
-def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None):
+def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, speculate=False):
     """Solve A x = rhs with right preconditioning A P^{-1} y = rhs, x = P^{-1} y.
 
     rhs: torch CUDA tensor (device path) or numpy array (bridged). Returns (x, KrylovReport) with x in
     the container type of rhs.
+
+    speculate (device path): enqueue iteration j+1's A P^{-1} v_{j+1} before waiting for iteration j's
+    Hessenberg column, so the host least-squares solve and the next launches overlap device work
+    (small problems are host-bound). Same arithmetic in the same stream order, so the iterates are
+    unchanged; the application issued after the last iteration is discarded and reported in
+    KrylovReport.speculative_applies.
     """
     if not (0.0 < rel_tol < 1.0):
         raise ValueError("rel_tol must lie in (0, 1)")
@@ -192,14 +199,32 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None):
     g[0] = beta
     k = 0
     happy = False
+    spec = bool(speculate) and not host and not complex_
+    if spec:
+        col_host = torch.empty(max_iter + 2, dtype=torch.float64, pin_memory=True)
+        col_ev = torch.cuda.Event()
+    w_next = None
     for j in range(max_iter):
-        w = A(P(basis[j])).clone()
+        w = w_next if w_next is not None else A(P(basis[j])).clone()
+        w_next = None
         # modified Gram-Schmidt: h_ij = <v_i, w>; w -= h_ij v_i  (fused pairwise on device)
         ops.mgs_step(w, None, None, basis[0], ops.hptr(0, j))
         for i in range(1, j + 1):
             ops.mgs_step(w, basis[i - 1], ops.hptr(i - 1, j), basis[i], ops.hptr(i, j))
         ops.mgs_step(w, basis[j], ops.hptr(j, j), None, ops.hptr(j + 1, j))
-        col = ops.col(j, j + 2)
+        if spec and j + 1 < max_iter:
+            # column j to pinned memory, then the next basis vector and its A P^{-1} product are queued
+            # behind it; the host waits only for the column
+            col_host[: j + 2].copy_(ops.H[j * ops.cols : j * ops.cols + j + 2], non_blocking=True)
+            col_ev.record()
+            vnext = torch.empty_like(b)
+            ops.scale_div(w, ops.hptr(j + 1, j), vnext)
+            w_next = A(P(vnext)).clone()
+            col_ev.synchronize()
+            col = col_host[: j + 2].numpy().copy()
+        else:
+            vnext = None
+            col = ops.col(j, j + 2)
         if not np.all(np.isfinite(col.view(np.float64) if complex_ else col)):
             raise NumericalFailureError("non-finite value in GMRES operator output")
         Hh[: j + 2, j] = col
@@ -207,12 +232,15 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None):
         if abs(Hh[j + 1, j]) < BREAKDOWN_TOL:
             happy = True
         else:
-            vnext = torch.empty_like(b)
-            ops.scale_div(w, ops.hptr(j + 1, j), vnext)
+            if vnext is None:
+                vnext = torch.empty_like(b)
+                ops.scale_div(w, ops.hptr(j + 1, j), vnext)
             basis.append(vnext)
         y, res = _solve_hessenberg(Hh[: k + 1, :k], g[: k + 1])
         report.residual_history.append(res)
         if happy or res <= target:
+            report.speculative_applies = 1 if w_next is not None else 0
+            w_next = None
             break
 
     y, _ = _solve_hessenberg(Hh[: k + 1, :k], g[: k + 1])
