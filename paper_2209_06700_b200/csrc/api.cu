@@ -23,6 +23,7 @@ struct spk_ctx {
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
+  int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
   // block-DoFs from which Chebyshev steps run split; launches of >= 3 blocks always run split (their
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
@@ -140,14 +141,20 @@ int ensure_scratch(spk_ctx* c, int need) {
   return SPK_OK;
 }
 
+// a level that is the whole mesh (no slab window)
+bool whole_level(const spk_ctx* c, int level) {
+  const SpkDims& g = c->dims[level];
+  return g.x0 == 0 && c->ex_begin[level] == 0 && (c->ex_end[level] == 0 || c->ex_end[level] == g.Ex) &&
+         c->store_last[level];
+}
+
 // whole-mesh 3D level that block-mode K1 launches run with the direct small-level kernel
 // (stage_apply.cuh launch_one: k <= 3 and n (2k+1)^3 <= SPK_SMALL_WORK)
 bool small_level(const spk_ctx* c, int level) {
   const SpkDims& g = c->dims[level];
   const long long w1 = 2LL * c->K + 1;
-  const bool whole = g.x0 == 0 && c->ex_begin[level] == 0 &&
-                     (c->ex_end[level] == 0 || c->ex_end[level] == g.Ex) && c->store_last[level];
-  return c->K <= 3 && c->dim == 3 && g.Ex > 0 && whole && g.n * w1 * w1 * w1 <= (long long)SPK_SMALL_WORK_HOST;
+  return c->K <= 3 && c->dim == 3 && g.Ex > 0 && whole_level(c, level) &&
+         g.n * w1 * w1 * w1 <= (long long)SPK_SMALL_WORK_HOST;
 }
 
 // x-chunking of the sliding window: enough CTAs to fill every SM about twice
@@ -323,6 +330,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
   if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
   if (const char* e = std::getenv("SPK_FILL_WAVE")) c->fill_wave = std::atoi(e);
+  if (const char* e = std::getenv("SPK_FUSE_TRANSFER")) c->fuse_transfer = std::atoi(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -756,6 +764,14 @@ int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in,
     for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
   const SpkDims gout = prolong ? gf : gc;
   const int lout = prolong ? level : level - 1;
+  // whole-mesh cubic 3D prolongation: one fused launch (vecops.cu prolong3d_kernel)
+  if (prolong && dim == 3 && c->fuse_transfer && whole_level(c, level) && whole_level(c, level - 1) &&
+      gc.Ex == gc.Ey && gc.Ex == gc.Ez) {
+    a.in = in; a.out = out; a.accumulate = accumulate; a.mask = mask; a.g = gout; a.Nc = Nc;
+    cudaError_t e = spk_launch_prolong3d(c->K, nblk, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "prolong3d");
+    return SPK_OK;
+  }
   int nsweeps = dim;
   for (int sw = 0; sw < nsweeps; ++sw) {
     const bool last = (sw == nsweeps - 1);

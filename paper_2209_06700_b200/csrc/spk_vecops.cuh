@@ -92,6 +92,7 @@ cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s);
 cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s);
 cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s);
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);
+cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s);
 int spk_mgs_grid();
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
