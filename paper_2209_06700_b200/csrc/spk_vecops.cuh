@@ -93,6 +93,7 @@ cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, in
 cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s);
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s);
+cudaError_t spk_launch_restrict3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s);
 int spk_mgs_grid();
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);

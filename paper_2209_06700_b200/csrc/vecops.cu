@@ -327,6 +327,76 @@ __global__ void __launch_bounds__(256) prolong3d_kernel(const __grid_constant__ 
   }
 }
 
+// ---- fused 3D restriction (whole-mesh cubic levels): out = mask((Px^T (x) Py^T (x) Pz^T) in) -------
+// One CTA per tile of E^3 coarse elements and block: the fine nodes the tile's coarse nodes gather
+// from (the tile plus 2K-1 fine planes on the low side) are loaded once, the z, y, x sweeps
+// (transfer_value, the three-sweep arithmetic) run in shared memory, the coarse tile is written once.
+template <int K>
+struct Restrict3 {
+  static constexpr int E = (K == 1) ? 4 : 2;
+  static constexpr int MCR = K * E + 1;          // coarse nodes per tile axis (incl. the domain end)
+  static constexpr int MFR = 2 * K * E + 2 * K;  // fine nodes per tile axis: [2K e0 - (2K-1), 2K e1]
+  static constexpr int SMEM = MFR * MFR * MFR + MFR * MFR * MCR + MFR * MCR * MCR;  // doubles
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) restrict3d_kernel(const __grid_constant__ SpkTransferArgs a) {
+  using G = Restrict3<K>;
+  constexpr int E = G::E, MC = G::MCR, MF = G::MFR, UNR = 4;
+  extern __shared__ double sm[];
+  double* Fs = sm;                 // [xf][yf][zf]
+  double* T1 = Fs + MF * MF * MF;  // [xf][yf][zc]
+  double* T2 = T1 + MF * MF * MC;  // [xf][yc][zc]
+  const int tid = threadIdx.x;
+  const int Nc = a.Nc, nc = K * Nc + 1, nf = 2 * K * Nc + 1;
+  const int nt = (Nc + E - 1) / E;
+  const int tz = blockIdx.x % nt, ty = blockIdx.x / nt, tx = blockIdx.y, b = blockIdx.z;
+  const int e0z = tz * E, e0y = ty * E, e0x = tx * E;
+  const int e1z = min(e0z + E, Nc), e1y = min(e0y + E, Nc), e1x = min(e0x + E, Nc);
+  const int mcz = K * (e1z - e0z) + (e1z == Nc), mcy = K * (e1y - e0y) + (e1y == Nc),
+            mcx = K * (e1x - e0x) + (e1x == Nc);
+  const int f0z = 2 * K * e0z - (2 * K - 1), f0y = 2 * K * e0y - (2 * K - 1), f0x = 2 * K * e0x - (2 * K - 1);
+  const double* fin = a.in + (long long)b * nf * nf * nf;
+  double* cout_ = a.out + (long long)b * nc * nc * nc;
+  for (int i0 = tid; i0 < MF * MF * MF; i0 += UNR * 256) {
+    double v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int idx = i0 + u * 256;
+      const int zf = idx % MF, t = idx / MF, yf = t % MF, xf = t / MF;
+      const int Z = f0z + zf, Y = f0y + yf, X = f0x + xf;
+      const bool on = idx < MF * MF * MF && Z >= 0 && Z < nf && Y >= 0 && Y < nf && X >= 0 && X < nf;
+      v[u] = on ? fin[((long long)X * nf + Y) * nf + Z] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (i0 + u * 256 < MF * MF * MF) Fs[i0 + u * 256] = v[u];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < MF * MF * MC; idx += blockDim.x) {  // z sweep
+    const int zc = idx % MC, t = idx / MC, yf = t % MF, xf = t / MF;
+    if (zc >= mcz) continue;
+    T1[idx] = transfer_value<K>(a, K * e0z + zc, Fs + (xf * MF + yf) * MF - f0z, 1);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < MF * MC * MC; idx += blockDim.x) {  // y sweep
+    const int zc = idx % MC, t = idx / MC, yc = t % MC, xf = t / MC;
+    if (zc >= mcz || yc >= mcy) continue;
+    T2[idx] = transfer_value<K>(a, K * e0y + yc, T1 + (long long)xf * MF * MC + zc - (long long)f0y * MC, MC);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < MC * MC * MC; idx += blockDim.x) {  // x sweep + mask + store
+    const int zc = idx % MC, t = idx / MC, yc = t % MC, xc = t / MC;
+    if (zc >= mcz || yc >= mcy || xc >= mcx) continue;
+    const int X = K * e0x + xc, Y = K * e0y + yc, Z = K * e0z + zc;
+    double val = transfer_value<K>(a, X, T2 + yc * MC + zc - (long long)f0x * MC * MC, (long long)MC * MC);
+    if (a.mask && bnd3(a.g, X, Y, Z)) val = 0.0;
+    double* dst = cout_ + ((long long)X * nc + Y) * nc + Z;
+    if (a.accumulate) val += *dst;
+    *dst = val;
+  }
+}
+
 // ---- pointwise Chebyshev kernels over the owned nodes [row0*nz, (row0+nrows)*nz) of a level:
 //      op 0 start (r = b, x = 0, d = Dinv r / theta), op 1 update after w = A d (r -= w; x += d;
 //      d = c1 d + c2 Dinv r), op 2 = op 1 fused with the final "return x + d" (multigrid.py:82-88)
@@ -750,6 +820,37 @@ cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cuda
   }
     SPK_P3(1) SPK_P3(2) SPK_P3(3) SPK_P3(4)
 #undef SPK_P3
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_restrict3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s) {
+  int E, smem;
+  switch (K) {
+    case 1: E = Restrict3<1>::E; smem = Restrict3<1>::SMEM; break;
+    case 2: E = Restrict3<2>::E; smem = Restrict3<2>::SMEM; break;
+    case 3: E = Restrict3<3>::E; smem = Restrict3<3>::SMEM; break;
+    case 4: E = Restrict3<4>::E; smem = Restrict3<4>::SMEM; break;
+    default: return cudaErrorInvalidValue;
+  }
+  const int nt = (a.Nc + E - 1) / E;
+  const dim3 grid((unsigned)(nt * nt), (unsigned)nt, (unsigned)nblk);
+  const size_t bytes = (size_t)smem * sizeof(double);
+  switch (K) {
+#define SPK_R3(KK)                                                                                    \
+  case KK: {                                                                                          \
+    static bool cfg = false;                                                                          \
+    if (!cfg) {                                                                                       \
+      cudaError_t e = cudaFuncSetAttribute(restrict3d_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)bytes);                                               \
+      if (e != cudaSuccess) return e;                                                                 \
+      cfg = true;                                                                                     \
+    }                                                                                                 \
+    restrict3d_kernel<KK><<<grid, 256, bytes, s>>>(a);                                                \
+    break;                                                                                            \
+  }
+    SPK_R3(1) SPK_R3(2) SPK_R3(3) SPK_R3(4)
+#undef SPK_R3
   }
   return cudaGetLastError();
 }
