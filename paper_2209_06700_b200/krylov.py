@@ -149,7 +149,8 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
     speculate (device path): enqueue iteration j+1's A P^{-1} v_{j+1} before waiting for iteration j's
     Hessenberg column, so the host least-squares solve and the next launches overlap device work
     (small problems are host-bound). Same arithmetic in the same stream order, so the iterates are
-    unchanged; the application issued after the last iteration is discarded and reported in
+    unchanged. Not done when the residual trend predicts convergence at the current iteration; an
+    application issued after the last iteration anyway is discarded and reported in
     KrylovReport.speculative_applies.
     """
     if not (0.0 < rel_tol < 1.0):
@@ -212,7 +213,11 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
         for i in range(1, j + 1):
             ops.mgs_step(w, basis[i - 1], ops.hptr(i - 1, j), basis[i], ops.hptr(i, j))
         ops.mgs_step(w, basis[j], ops.hptr(j, j), None, ops.hptr(j + 1, j))
-        if spec and j + 1 < max_iter:
+        # skip the speculation when the residual trend predicts convergence at this iteration (the
+        # product would be discarded; a wrong guess only loses the overlap of one iteration)
+        hist = report.residual_history
+        likely_last = len(hist) >= 2 and hist[-2] > 0 and hist[-1] * (hist[-1] / hist[-2]) <= target
+        if spec and j + 1 < max_iter and not likely_last:
             # column j to pinned memory, then the next basis vector and its A P^{-1} product are queued
             # behind it; the host waits only for the column
             col_host[: j + 2].copy_(ops.H[j * ops.cols : j * ops.cols + j + 2], non_blocking=True)
