@@ -296,33 +296,36 @@ __global__ void __launch_bounds__(256) prolong3d_kernel(const __grid_constant__ 
     T2[(ix * MF + yf) * MF + zf] = val;
   }
   __syncthreads();
-  for (int i0 = tid; i0 < MF * MF * MF; i0 += UNR * 256) {  // x sweep + store (batched accumulate loads)
-    double old[UNR];
-    double* dst[UNR];
-    bool on[UNR];
+  // x sweep + store: a thread owns (yf, zf) columns and walks x, the accumulate loads of UNR planes
+  // issued together (the position along x, hence the table row, is uniform across the CTA)
+  for (int p = tid; p < MF * MF; p += blockDim.x) {
+    const int zf = p % MF, yf = p / MF;
+    if (zf >= mfz || yf >= mfy) continue;
+    const int Y = 2 * K * e0y + yf, Z = 2 * K * e0z + zf;
+    double* col = fout + (long long)Y * nf + Z;
+    const double* tcol = T2 + yf * MF + zf;
+    const long long plane = (long long)nf * nf;
+    for (int x0 = 0; x0 < mfx; x0 += UNR) {
+      double old[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int idx = i0 + u * 256;
-      const int zf = idx % MF, t = idx / MF, yf = t % MF, xf = t / MF;
-      on[u] = idx < MF * MF * MF && zf < mfz && yf < mfy && xf < mfx;
-      const int X = 2 * K * e0x + xf, Y = 2 * K * e0y + yf, Z = 2 * K * e0z + zf;
-      dst[u] = fout + ((long long)X * nf + Y) * nf + Z;
-      old[u] = (on[u] && a.accumulate) ? *dst[u] : 0.0;
-    }
+      for (int u = 0; u < UNR; ++u) {
+        const int xf = x0 + u;
+        old[u] = (xf < mfx && a.accumulate) ? col[(long long)(2 * K * e0x + xf) * plane] : 0.0;
+      }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (!on[u]) continue;
-      const int idx = i0 + u * 256;
-      const int zf = idx % MF, t = idx / MF, yf = t % MF, xf = t / MF;
-      int base, f;
-      locate(2 * K * e0x + xf, e0x, base, f);
-      const double* src = T2 + (base * MF + yf) * MF + zf;
-      double val = 0.0;
+      for (int u = 0; u < UNR; ++u) {
+        const int xf = x0 + u;
+        if (xf >= mfx) break;
+        int base, f;
+        locate(2 * K * e0x + xf, e0x, base, f);
+        double val = 0.0;
 #pragma unroll
-      for (int j = 0; j <= K; ++j) val = fma(a.P[f * PS + j], src[(long long)j * MF * MF], val);
-      if (a.mask && bnd3(a.g, 2 * K * e0x + xf, 2 * K * e0y + yf, 2 * K * e0z + zf)) val = 0.0;
-      if (a.accumulate) val += old[u];
-      *dst[u] = val;
+        for (int j = 0; j <= K; ++j) val = fma(a.P[f * PS + j], tcol[(base + j) * MF * MF], val);
+        const int X = 2 * K * e0x + xf;
+        if (a.mask && bnd3(a.g, X, Y, Z)) val = 0.0;
+        if (a.accumulate) val += old[u];
+        col[(long long)X * plane] = val;
+      }
     }
   }
 }
