@@ -24,6 +24,7 @@ struct spk_ctx {
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
+  long long fuse_restrict_max = 1LL << 22;  // fused 3D restriction up to nblk * n fine DoFs (SPK_FUSE_RESTRICT_MAX)
   // block-DoFs from which Chebyshev steps run split; launches of >= 3 blocks always run split (their
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
@@ -331,6 +332,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
   if (const char* e = std::getenv("SPK_FILL_WAVE")) c->fill_wave = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_TRANSFER")) c->fuse_transfer = std::atoi(e);
+  if (const char* e = std::getenv("SPK_FUSE_RESTRICT_MAX")) c->fuse_restrict_max = std::atoll(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -767,7 +769,7 @@ int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in,
   // whole-mesh cubic 3D levels: one fused launch (vecops.cu prolong3d_kernel / restrict3d_kernel)
   // (restriction only on launch-bound levels: on large ones its fine-tile halo re-reads make the
   // three streaming sweeps faster, measured: C4 finest level 399 vs 950 us)
-  const bool fuse_r = (long long)nblk * gf.n <= (1LL << 22);
+  const bool fuse_r = (long long)nblk * gf.n <= c->fuse_restrict_max;
   if (dim == 3 && c->fuse_transfer && (prolong || fuse_r) && whole_level(c, level) && whole_level(c, level - 1) &&
       gc.Ex == gc.Ey && gc.Ex == gc.Ez) {
     a.in = in; a.out = out; a.accumulate = accumulate; a.mask = mask; a.g = gout; a.Nc = Nc;
