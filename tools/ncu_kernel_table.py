@@ -10,7 +10,7 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_elapsed.avg.per_second"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 out = open(sys.argv[1], "w")
-out.write("# ncu --set full --clock-control none, one launch per kernel (one B200); tools/_ncu_kernels.sh\n"
+out.write("# ncu --set full --clock-control none, one launch per kernel (one B200); tools/ncu_kernels.sh\n"
           "# DRAM GB/s = (read + write) / duration. HBM-bound kernels are judged against 6546.6 GB/s (MEASURED_PEAKS);\n"
           "# K1 launches by the FP64 pipe (34.2 TF/s measured DFMA peak) -- see DESIGN.md §3\n")
 for arg in sys.argv[2:]:

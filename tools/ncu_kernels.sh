@@ -1,3 +1,4 @@
+# ncu --set full of one launch of every step-path kernel at full size, summarised on the box (reports are large)
 N="ncu --set full --clock-control none --import-source on -f"
 $N -k regex:mgs_kernel -s 3 -c 1 -o gpurun_out/kr_mgs python tools/prof_mgs.py > /dev/null 2>&1
 $N -k regex:combine_small_kernel -s 3 -c 1 -o gpurun_out/kr_combine python tools/prof_combine.py > /dev/null 2>&1
