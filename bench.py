@@ -65,7 +65,7 @@ def config_dict(args, world, extra=None):
     return d
 
 
-def radau_step_sample(steps=4):
+def radau_step_sample(steps=4, cpu=True):
     """Time per Radau IIA step of C3 (BASELINE.json configs[2]: 32^3 Q2 hex, Q=3, tau=0.01, GMRES
     rtol 1e-12, Chebyshev degree 3) on this GPU: the second half of the metric ("time per Radau IIA
     step"). Device-resident state, CUDA events around `steps` steps after one warm-up step."""
@@ -88,10 +88,33 @@ def radau_step_sample(steps=4):
         its.append(rep.iterations)
     e1.record()
     torch.cuda.synchronize()
-    return {"config": "C3 (32^3 Q2 hex, Radau IIA Q=3, tau=0.01, rtol 1e-12, Chebyshev deg 3)",
-            "ms_per_step": e0.elapsed_time(e1) / steps, "steps": steps, "gmres_iterations": its,
-            "n_gpus": 1, "note": "per-config step times (C1, C3, C4, C5): tools/bench_steps.py, "
-                                 "profiles/r01_steps.jsonl"}
+    out = {"config": "C3 (32^3 Q2 hex, Radau IIA Q=3, tau=0.01, rtol 1e-12, Chebyshev deg 3)",
+           "ms_per_step": e0.elapsed_time(e1) / steps, "steps": steps, "gmres_iterations": its,
+           "n_gpus": 1, "note": "per-config step times (C1, C3, C4, C5): tools/bench_steps.py, "
+                                "profiles/r01_steps.jsonl"}
+    if cpu:
+        out["cpu_baseline"] = cpu_step_sample(tau)
+    return out
+
+
+def cpu_step_sample(tau):
+    """The oracle (the reference's algorithm: dense-1D contractions, numpy) running the same C3 step
+    on all host cores: one step after setup (~5-10 s)."""
+    import threadpoolctl
+    from oracle import solvers as OS
+    from oracle import stepper as OST
+    from oracle.fem_qk import Hierarchy
+    from oracle.tableau_ref import radau_iia as ref_radau
+
+    cores = len(os.sched_getaffinity(0))
+    with threadpoolctl.threadpool_limits(cores):
+        ora = OST.RealLU(Hierarchy(3, 5, 2), 3, tau, OS.Config(smoother_degree=3), tab=ref_radau(3))
+        uo = ora.initial()
+        t0 = time.perf_counter()
+        uo, its, _ = ora.step(0.0, uo)
+        dt = time.perf_counter() - t0
+    return {"ms_per_step": dt * 1e3, "cores": cores, "kind": "port", "gmres_iterations": its,
+            "sample": "one C3 step of the oracle (first step from the initial condition)"}
 
 
 def cpu_sample(Q, degree, tau, seconds=10.0):
@@ -296,7 +319,7 @@ def run_ours(args):
 
     step = None
     if rank == 0 and world == 1 and not args.no_step:
-        step = radau_step_sample()
+        step = radau_step_sample(cpu=not args.no_cpu)
 
     if rank == 0:
         launches_per_apply = 1 if op is None else op.launches_per_apply
