@@ -144,6 +144,11 @@ int spk_cheb_split(spk_ctx* ctx, int level, int nblk);
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
             const double* v_cur, double* out, void* stream);
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);
+/* One MGS column (krylov.py:74-82) in one call: the j+2 fused spk_mgs sweeps of w against basis[0..j]
+ * (host array of device pointers), H[0..j+1, j] written to hcol (device), then v_next = w / H[j+1, j]
+ * when v_next is not NULL. Same launches and order as the per-sweep calls. */
+int spk_mgs_column(spk_ctx* ctx, long long n, int j, const double* const* basis, double* w, double* hcol,
+                   double* v_next, void* stream);
 int spk_lincomb(long long n, int k, const double* const* vs_dev, const double* y_dev, double* z,
                 void* stream);
 

@@ -71,6 +71,7 @@ _SIGS = {
     "spk_copy_d2d": ([c_vp, c_vp, c_ll, c_vp], c_int),
     "spk_mgs": ([c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_scale_div": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),
+    "spk_mgs_column": ([c_vp, c_ll, c_int, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_lincomb": ([c_ll, c_int, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_outer3": ([c_vp, c_int, c_vp, c_vp, c_vp], c_int),
     "spk_rhs": ([c_vp, c_int, c_int, c_vp, P_dbl, P_dbl, c_vp, c_vp, c_vp], c_int),

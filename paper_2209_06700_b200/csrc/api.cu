@@ -909,6 +909,19 @@ int spk_mgs(spk_ctx* c, long long n, double* w, const double* v_prev, const doub
   return SPK_OK;
 }
 
+int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, double* w, double* hcol,
+                   double* v_next, void* stream) {
+  // column j of modified Gram-Schmidt (krylov.py:74-82) as one call: j+2 fused sweeps, then
+  // v_{j+1} = w / h_{j+1,j}; hcol points at H[0, j] (H[i, j] = hcol[i], device-resident)
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (j < 0 || !basis || !w || !hcol) return fail(SPK_ECONFIG, "mgs_column: bad arguments");
+  int rc = spk_mgs(c, n, w, nullptr, nullptr, basis[0], hcol, stream);
+  for (int i = 1; rc == SPK_OK && i <= j; ++i) rc = spk_mgs(c, n, w, basis[i - 1], hcol + i - 1, basis[i], hcol + i, stream);
+  if (rc == SPK_OK) rc = spk_mgs(c, n, w, basis[j], hcol + j, nullptr, hcol + j + 1, stream);
+  if (rc == SPK_OK && v_next) rc = spk_scale_div(n, w, hcol + j + 1, v_next, stream);
+  return rc;
+}
+
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream) {
   cudaError_t e = spk_launch_scale_div(n, w, h, v, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "scale_div");

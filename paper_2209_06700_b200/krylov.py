@@ -205,14 +205,23 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
         col_host = torch.empty(max_iter + 2, dtype=torch.float64, pin_memory=True)
         col_ev = torch.cuda.Event()
     w_next = None
+    # real device path: one C call per MGS column (the j+2 fused sweeps and v_{j+1} = w / h)
+    basis_ptrs = (_lib.ctypes.c_void_p * (max_iter + 1))() if not complex_ else None
     for j in range(max_iter):
         w = w_next if w_next is not None else A(P(basis[j])).clone()
         w_next = None
-        # modified Gram-Schmidt: h_ij = <v_i, w>; w -= h_ij v_i  (fused pairwise on device)
-        ops.mgs_step(w, None, None, basis[0], ops.hptr(0, j))
-        for i in range(1, j + 1):
-            ops.mgs_step(w, basis[i - 1], ops.hptr(i - 1, j), basis[i], ops.hptr(i, j))
-        ops.mgs_step(w, basis[j], ops.hptr(j, j), None, ops.hptr(j + 1, j))
+        vcol = None
+        if not complex_:
+            basis_ptrs[j] = basis[j].data_ptr()
+            vcol = torch.empty_like(b)
+            _lib.call("spk_mgs_column", ops.ctx, n, j, _lib.ctypes.addressof(basis_ptrs), ptr(w), ops.hptr(0, j),
+                      ptr(vcol), ops.st)
+        else:
+            # modified Gram-Schmidt: h_ij = <v_i, w>; w -= h_ij v_i  (fused pairwise on device)
+            ops.mgs_step(w, None, None, basis[0], ops.hptr(0, j))
+            for i in range(1, j + 1):
+                ops.mgs_step(w, basis[i - 1], ops.hptr(i - 1, j), basis[i], ops.hptr(i, j))
+            ops.mgs_step(w, basis[j], ops.hptr(j, j), None, ops.hptr(j + 1, j))
         # skip the speculation when the residual trend predicts convergence at this iteration (the
         # product would be discarded; a wrong guess only loses the overlap of one iteration)
         hist = report.residual_history
@@ -222,13 +231,12 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
             # behind it; the host waits only for the column
             col_host[: j + 2].copy_(ops.H[j * ops.cols : j * ops.cols + j + 2], non_blocking=True)
             col_ev.record()
-            vnext = torch.empty_like(b)
-            ops.scale_div(w, ops.hptr(j + 1, j), vnext)
+            vnext = vcol
             w_next = A(P(vnext)).clone()
             col_ev.synchronize()
             col = col_host[: j + 2].numpy().copy()
         else:
-            vnext = None
+            vnext = vcol
             col = ops.col(j, j + 2)
         if not np.all(np.isfinite(col.view(np.float64) if complex_ else col)):
             raise NumericalFailureError("non-finite value in GMRES operator output")
