@@ -144,6 +144,15 @@ int spk_cheb_split(spk_ctx* ctx, int level, int nblk);
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
             const double* v_cur, double* out, void* stream);
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);
+/* Fused V-cycle on levels 0..lc (multigrid.py:110-140 with the direct coarse solve, block family):
+ * x_lc = V-cycle(b_lc) for nblk blocks in one launch (one CTA per block, level vectors in shared
+ * memory). coef: device [lc+1][nblk][1 + 2(deg-1)] (theta, then c1, c2 per inner Chebyshev step);
+ * cinv: device (nblk, n0, n0) inverse of the constrained coarse operator; flags: device int per level.
+ * spk_coarse_vcycle_level returns the highest fusable level (-1: none). */
+int spk_coarse_vcycle_level(spk_ctx* ctx);
+int spk_coarse_vcycle(spk_ctx* ctx, int lc, int nblk, const double* lams, double tau, int deg,
+                      const double* coef, const double* cinv, const double* b, double* x, int* flags,
+                      void* stream);
 /* One MGS column (krylov.py:74-82) in one call: the j+2 fused spk_mgs sweeps of w against basis[0..j]
  * (host array of device pointers), H[0..j+1, j] written to hcol (device), then v_next = w / H[j+1, j]
  * when v_next is not NULL. Same launches and order as the per-sweep calls. */

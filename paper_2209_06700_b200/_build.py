@@ -14,7 +14,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "_spk.so")
 OBJDIR = os.path.join(HERE, "_obj")
 SOURCES = ["stage_apply.cu", "stage_apply_k1.cu", "stage_apply_k2.cu", "stage_apply_k3.cu",
-           "stage_apply_k4.cu", "vecops.cu", "api.cu"]
+           "stage_apply_k4.cu", "vecops.cu", "coarse_vcycle.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

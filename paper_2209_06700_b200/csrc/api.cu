@@ -909,6 +909,39 @@ int spk_mgs(spk_ctx* c, long long n, double* w, const double* v_prev, const doub
   return SPK_OK;
 }
 
+int spk_coarse_vcycle_level(spk_ctx* c) {
+  if (!c || c->dim != 3) return -1;
+  int best = -1;
+  for (int l = 1; l <= c->max_level && l <= SPK_CV_LMAX; ++l) {
+    if (!whole_level(c, l) || !whole_level(c, l - 1)) break;
+    if (spk_coarse_vcycle_smem(c->K, l) > SPK_CV_SMEM_MAX) break;
+    best = l;
+  }
+  return best;
+}
+
+int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double tau, int deg, const double* coef,
+                      const double* cinv, const double* b, double* x, int* flags, void* stream) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (lc < 1 || lc > spk_coarse_vcycle_level(c)) return fail(SPK_ECONFIG, "coarse_vcycle: level not fusable");
+  if (nblk < 1 || nblk > SPK_BMAX || deg < 1 || deg > 8) return fail(SPK_ECONFIG, "coarse_vcycle: bad sizes");
+  SpkCoarseArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.lc = lc; a.nblk = nblk; a.deg = deg; a.tau = tau;
+  for (int i = 0; i < nblk; ++i) a.lam[i] = lams[i];
+  for (int l = 0; l <= lc; ++l) {
+    a.hd[l] = std::pow(c->h[l], 3);
+    a.hk[l] = c->h[l];
+  }
+  for (int f = 0; f <= 2 * c->K; ++f)
+    for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
+  a.coef = coef; a.cinv = cinv; a.b = b; a.x = x; a.flags = flags;
+  a.sb = c->dims[lc].n; a.sx = c->dims[lc].n;
+  cudaError_t e = spk_launch_coarse_vcycle(c->K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "coarse_vcycle");
+  return SPK_OK;
+}
+
 int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, double* w, double* hcol,
                    double* v_next, void* stream) {
   // column j of modified Gram-Schmidt (krylov.py:74-82) as one call: j+2 fused sweeps, then

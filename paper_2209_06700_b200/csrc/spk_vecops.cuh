@@ -91,6 +91,26 @@ struct SpkRhsArgs {
 cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s);
 cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s);
 cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_t s);
+// fused coarse-level V-cycle (coarse_vcycle.cu): levels 0..lc of a whole-mesh 3D hierarchy, one CTA
+// per block, all level vectors in shared memory
+#define SPK_CV_LMAX 4
+#define SPK_CV_SMEM_MAX (200 * 1024)
+struct SpkCoarseArgs {
+  int lc, nblk, deg;
+  double tau;
+  double lam[SPK_BMAX];                            // block shifts (unscaled)
+  double hd[SPK_CV_LMAX + 1], hk[SPK_CV_LMAX + 1];  // h^3, h per level
+  double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];   // 1D prolongation table
+  const double* coef;  // [lc+1][nblk][1 + 2(deg-1)]: theta, (c1, c2) per inner step
+  const double* cinv;  // (nblk, n0, n0) row-major inverse of the constrained coarse operator
+  const double* b;     // rhs at level lc, block stride sb
+  double* x;           // result at level lc, block stride sx
+  int* flags;          // per-level NaN flags
+  long long sb, sx;
+};
+long long spk_coarse_vcycle_smem(int K, int lc);
+cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t s);
+
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s);
 cudaError_t spk_launch_restrict3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s);

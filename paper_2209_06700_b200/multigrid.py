@@ -21,6 +21,8 @@ the same launches: numerically identical to Q separate BlockSolvers, Q times few
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import scipy.linalg
 import torch
@@ -126,6 +128,10 @@ class _DeviceVCycle:
     """V-cycle engine over nblk independent blocks (or one 2x2 pair) on the device."""
 
     pair = False
+    # the coarsest levels (a few thousand nodes per block) run as ONE fused launch
+    # (spk_coarse_vcycle: the same cycle inside one CTA per block, vectors in shared memory)
+    _fuse_coarse = os.environ.get("SPK_FUSE_COARSE", "1") != "0"
+    _cv_level = -1
 
     def __init__(self, hierarchy, config, min_level):
         if not (0 <= min_level <= hierarchy.max_level):
@@ -243,6 +249,26 @@ class _DeviceVCycle:
         for level in range(self.min_level, h.max_level + 1):
             self._bufs[level] = _Level(self.nrows, h.levels[level].n_dofs, h.device, level < h.max_level)
         self._flags = torch.zeros(h.max_level + 1, dtype=torch.int32, device=h.device)
+        self._cv_level = -1
+        if (self._fuse_coarse and not self.pair and h.dim == 3 and self.min_level == 0
+                and self.config.coarse_solver == "direct" and self.nrows <= 16):
+            lc = min(int(_lib.load().spk_coarse_vcycle_level(h.ctx)), h.max_level)
+            if lc >= 1:
+                deg = self.config.smoother_degree
+                rows = []
+                for level in range(lc + 1):
+                    for b in range(self.nrows):
+                        if level == 0:
+                            rows.append([0.0] * (2 * deg - 1))
+                            continue
+                        sm = self._level_smoothers(level)[b]
+                        row = [sm.theta]
+                        for c1, c2 in sm.coefficients():
+                            row += [c1, c2]
+                        rows.append(row)
+                self._cv_coef = torch.tensor(rows, dtype=torch.float64, device=h.device).contiguous()
+                self._cv_lams = _lib.dbl_array(self._block_lams())
+                self._cv_level = lc
 
     def _coarse(self, b):
         """Coarse solve: direct (inverse of the assembled coarse operator) or Chebyshev."""
@@ -286,7 +312,20 @@ class _DeviceVCycle:
             invs.append(scipy.linalg.lu_solve(lu, np.eye(nc)))
         return torch.from_numpy(np.stack(invs)).to(h.device)
 
+    def _coarse_fused(self, level, b):
+        """Levels 0..level in one launch (spk_coarse_vcycle)."""
+        h = self.hierarchy
+        lv = self._bufs[level]
+        if self._coarse_inv is None:
+            self._coarse_inv = self._build_coarse_inverse().contiguous()
+        _lib.call("spk_coarse_vcycle", h.ctx, level, self.nrows, self._cv_lams, self.tau,
+                  self.config.smoother_degree, ptr(self._cv_coef), ptr(self._coarse_inv), ptr(b), ptr(lv.x),
+                  ptr(self._flags), stream_ptr(h.device))
+        return lv.x
+
     def _cycle(self, level, b):
+        if level == self._cv_level:
+            return self._coarse_fused(level, b)
         if level == self.min_level:
             return self._coarse(b)
         lv = self._bufs[level]

@@ -262,6 +262,8 @@ class DistMultiBlockSolver(_BlockFamily):
     operator and start vector); finer levels run the power iteration on the slabs with the norms
     all-reduced over the column group (sqrt of the summed squares)."""
 
+    _fuse_coarse = False  # windowed levels: the replica coarse cycle (self.rep) fuses instead
+
     def __init__(self, slab_h, lams, tau, config=None):
         self.part = slab_h.part
         self.rep = MultiBlockSolver(GridHierarchy(3, self.part.gather_level, slab_h.degree, slab_h.device),
