@@ -147,12 +147,13 @@ int spk_scale_div(long long n, const double* w, const double* h, double* v, void
 /* Fused V-cycle on levels 0..lc (multigrid.py:110-140 with the direct coarse solve, block family):
  * x_lc = V-cycle(b_lc) for nblk blocks in one launch (one CTA per block, level vectors in shared
  * memory). coef: device [lc+1][nblk][1 + 2(deg-1)] (theta, then c1, c2 per inner Chebyshev step);
- * cinv: device (nblk, n0, n0) inverse of the constrained coarse operator; flags: device int per level.
+ * cinv: device (nblk, n0, n0) inverse of the constrained coarse operator; scratch: device
+ * nblk * 3 * n_lc doubles (r, d, w); flags: device int per level.
  * spk_coarse_vcycle_level returns the highest fusable level (-1: none). */
 int spk_coarse_vcycle_level(spk_ctx* ctx);
 int spk_coarse_vcycle(spk_ctx* ctx, int lc, int nblk, const double* lams, double tau, int deg,
-                      const double* coef, const double* cinv, const double* b, double* x, int* flags,
-                      void* stream);
+                      const double* coef, const double* cinv, const double* b, double* x, double* scratch,
+                      int* flags, void* stream);
 /* One MGS column (krylov.py:74-82) in one call: the j+2 fused spk_mgs sweeps of w against basis[0..j]
  * (host array of device pointers), H[0..j+1, j] written to hcol (device), then v_next = w / H[j+1, j]
  * when v_next is not NULL. Same launches and order as the per-sweep calls. */

@@ -73,7 +73,8 @@ _SIGS = {
     "spk_scale_div": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_mgs_column": ([c_vp, c_ll, c_int, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_coarse_vcycle_level": ([c_vp], c_int),
-    "spk_coarse_vcycle": ([c_vp, c_int, c_int, P_dbl, c_dbl, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "spk_coarse_vcycle": ([c_vp, c_int, c_int, P_dbl, c_dbl, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+                          c_int),
     "spk_lincomb": ([c_ll, c_int, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_outer3": ([c_vp, c_int, c_vp, c_vp, c_vp], c_int),
     "spk_rhs": ([c_vp, c_int, c_int, c_vp, P_dbl, P_dbl, c_vp, c_vp, c_vp], c_int),

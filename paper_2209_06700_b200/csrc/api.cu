@@ -24,6 +24,8 @@ struct spk_ctx {
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
+  long long cv_max_nodes = 2200;  // fused coarse V-cycle: top level up to this many nodes (SPK_CV_MAXN;
+                                  // measured: a single CTA loses at 17^3 nodes, k=2 C3 V-cycle 479 vs 569 us)
   long long fuse_restrict_max = 1LL << 22;  // fused 3D restriction up to nblk * n fine DoFs (SPK_FUSE_RESTRICT_MAX)
   // block-DoFs from which Chebyshev steps run split; launches of >= 3 blocks always run split (their
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
@@ -333,6 +335,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (const char* e = std::getenv("SPK_FILL_WAVE")) c->fill_wave = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_TRANSFER")) c->fuse_transfer = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_RESTRICT_MAX")) c->fuse_restrict_max = std::atoll(e);
+  if (const char* e = std::getenv("SPK_CV_MAXN")) c->cv_max_nodes = std::atoll(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -914,14 +917,14 @@ int spk_coarse_vcycle_level(spk_ctx* c) {
   int best = -1;
   for (int l = 1; l <= c->max_level && l <= SPK_CV_LMAX; ++l) {
     if (!whole_level(c, l) || !whole_level(c, l - 1)) break;
-    if (spk_coarse_vcycle_smem(c->K, l) > SPK_CV_SMEM_MAX) break;
+    if (spk_coarse_vcycle_smem(c->K, l) > SPK_CV_SMEM_MAX || c->dims[l].n > c->cv_max_nodes) break;
     best = l;
   }
   return best;
 }
 
 int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double tau, int deg, const double* coef,
-                      const double* cinv, const double* b, double* x, int* flags, void* stream) {
+                      const double* cinv, const double* b, double* x, double* scratch, int* flags, void* stream) {
   if (!c) return fail(SPK_ECONFIG, "null context");
   if (lc < 1 || lc > spk_coarse_vcycle_level(c)) return fail(SPK_ECONFIG, "coarse_vcycle: level not fusable");
   if (nblk < 1 || nblk > SPK_BMAX || deg < 1 || deg > 8) return fail(SPK_ECONFIG, "coarse_vcycle: bad sizes");
@@ -935,7 +938,8 @@ int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double t
   }
   for (int f = 0; f <= 2 * c->K; ++f)
     for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];
-  a.coef = coef; a.cinv = cinv; a.b = b; a.x = x; a.flags = flags;
+  if (!scratch) return fail(SPK_ECONFIG, "coarse_vcycle: scratch (nblk * 3 * n_lc doubles) required");
+  a.coef = coef; a.cinv = cinv; a.b = b; a.x = x; a.flags = flags; a.scratch = scratch;
   a.sb = c->dims[lc].n; a.sx = c->dims[lc].n;
   cudaError_t e = spk_launch_coarse_vcycle(c->K, a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "coarse_vcycle");

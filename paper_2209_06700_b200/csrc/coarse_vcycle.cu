@@ -3,8 +3,9 @@
 //
 // Below a few thousand nodes per block every kernel of the V-cycle (multigrid.py:110-140: Chebyshev
 // steps, residual, restriction, prolongation, the coarse solve) is a launch of a few microseconds
-// of latency: a level costs ~13 launches. Here levels 0..lc of one block run inside ONE CTA with all
-// level vectors in shared memory: the same sequence of operations (multigrid._DeviceVCycle._cycle /
+// of latency: a level costs ~13 launches. Here levels 0..lc of one block run inside ONE CTA (the
+// vectors of the levels below lc and the operator's sweep buffers in shared memory, level lc's
+// vectors in global memory / L2): the same sequence of operations (multigrid._DeviceVCycle._cycle /
 // _smooth / ChebyshevSmoother.apply, reference multigrid.py:65-140) with the operator applied by sum
 // factorisation over the assembled 1D band rows, the transfers as three in-smem sweeps
 // (vecops.cu transfer_value arithmetic) and the coarse level as the dense inverse (multigrid.py:
@@ -257,29 +258,31 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   extern __shared__ double sm[];
   const int blk = blockIdx.x;
   const int lc = a.lc;
+  // shared memory: the operator's four sweep buffers at the top level's size and every vector of the
+  // levels below lc; level lc's x and b are the caller's arrays and r, d, w (all levels) live in a
+  // per-block global scratch -- L2-resident, so the top level may be larger than the smem budget
+  // would allow for all nine of its vectors
   CVShared S;
-  double* p = sm;
-  for (int l = 0; l <= lc; ++l) {
-    const CVLevel<K> L(l);
-    S.X[l] = p; p += L.n;
-    S.B[l] = p; p += L.n;
-  }
   const int nmax = CVLevel<K>(lc).n;
-  S.R = p; p += nmax;
-  S.D = p; p += nmax;
-  S.W = p; p += nmax;
+  double* p = sm;
   S.T0 = p; p += nmax;
   S.T1 = p; p += nmax;
   S.T2 = p; p += nmax;
   S.T3 = p; p += nmax;
+  for (int l = 0; l < lc; ++l) {
+    const CVLevel<K> L(l);
+    S.X[l] = p; p += L.n;
+    S.B[l] = p; p += L.n;
+  }
+  S.X[lc] = a.x + (long long)blk * a.sx;
+  S.B[lc] = const_cast<double*>(a.b) + (long long)blk * a.sb;
+  double* scr = a.scratch + (long long)blk * 3 * nmax;
+  S.R = scr;
+  S.D = scr + nmax;
+  S.W = scr + 2 * nmax;
   S.bm = bm;
   S.bk = bk;
   Band<K>::build(bm, bk);
-  {
-    const int n = CVLevel<K>(lc).n;
-    const double* src = a.b + (long long)blk * a.sb;
-    for (int i = threadIdx.x; i < n; i += CV_NT) S.B[lc][i] = src[i];
-  }
   __syncthreads();
   const double lam = a.lam[blk];
   bool bad[SPK_CV_LMAX + 1];
@@ -312,11 +315,6 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
     cv_prolong<K>(S, a.P, l);
     cv_smooth<K>(S, a, l, blk, false, lamp, taup, bad[l]);
   }
-  {
-    const int n = CVLevel<K>(lc).n;
-    double* dst = a.x + (long long)blk * a.sx;
-    for (int i = threadIdx.x; i < n; i += CV_NT) dst[i] = S.X[lc][i];
-  }
   if (a.flags) {
     for (int l = 1; l <= lc; ++l)
       if (bad[l]) atomicOr(a.flags + l, 1);
@@ -326,13 +324,13 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
 }  // namespace
 
 long long spk_coarse_vcycle_smem(int K, int lc) {
-  long long tot = 0, nmax = 0;
-  for (int l = 0; l <= lc; ++l) {
-    const long long m = ((long long)K << l) + 1, n = m * m * m;
-    tot += 2 * n;
-    nmax = n;
+  long long tot = 0;
+  for (int l = 0; l < lc; ++l) {
+    const long long m = ((long long)K << l) + 1;
+    tot += 2 * m * m * m;
   }
-  return (tot + 7 * nmax) * (long long)sizeof(double);
+  const long long m = ((long long)K << lc) + 1;
+  return (tot + 4 * m * m * m) * (long long)sizeof(double);
 }
 
 cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t s) {

@@ -106,6 +106,7 @@ struct SpkCoarseArgs {
   const double* b;     // rhs at level lc, block stride sb
   double* x;           // result at level lc, block stride sx
   int* flags;          // per-level NaN flags
+  double* scratch;     // (nblk, 3, n_lc): r, d, w of every level (global, L2-resident)
   long long sb, sx;
 };
 long long spk_coarse_vcycle_smem(int K, int lc);

@@ -268,6 +268,8 @@ class _DeviceVCycle:
                         rows.append(row)
                 self._cv_coef = torch.tensor(rows, dtype=torch.float64, device=h.device).contiguous()
                 self._cv_lams = _lib.dbl_array(self._block_lams())
+                self._cv_scratch = torch.zeros((self.nrows, 3 * h.levels[lc].n_dofs), dtype=torch.float64,
+                                               device=h.device)
                 self._cv_level = lc
 
     def _coarse(self, b):
@@ -320,7 +322,7 @@ class _DeviceVCycle:
             self._coarse_inv = self._build_coarse_inverse().contiguous()
         _lib.call("spk_coarse_vcycle", h.ctx, level, self.nrows, self._cv_lams, self.tau,
                   self.config.smoother_degree, ptr(self._cv_coef), ptr(self._coarse_inv), ptr(b), ptr(lv.x),
-                  ptr(self._flags), stream_ptr(h.device))
+                  ptr(self._cv_scratch), ptr(self._flags), stream_ptr(h.device))
         return lv.x
 
     def _cycle(self, level, b):
