@@ -316,6 +316,26 @@ bool cheb_split(const spk_ctx* c, int level, int nblk) {
 
 }  // namespace
 
+bool spk_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("SPK_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+long long spk_pdl_max_ctas() {
+  // measured: PDL pays on latency-bound launches (one wave) and costs on large grids (C4 V-cycle
+  // +10 % with every launch of up to 8 CTAs per SM attributed)
+  static long long m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("SPK_PDL_MAX");
+    m = e ? std::atoll(e) : 148;
+  }
+  return m;
+}
+
 extern "C" {
 
 int spk_version(void) { return 1; }

@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   S.bm = bm;
   S.bk = bk;
   Band<K>::build(bm, bk);
+  spk_pdl_wait();
   __syncthreads();
   const double lam = a.lam[blk];
   bool bad[SPK_CV_LMAX + 1];
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
     cv_prolong<K>(S, a.P, l);
     cv_smooth<K>(S, a, l, blk, false, lamp, taup, bad[l]);
   }
+  spk_pdl_trigger();  // at the end: dependents parked early would share this CTA's SM for its whole run
   if (a.flags) {
     for (int l = 1; l <= lc; ++l)
       if (bad[l]) atomicOr(a.flags + l, 1);
@@ -346,8 +348,7 @@ cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t
       if (e != cudaSuccess) return e;                                                                \
       cfg = true;                                                                                    \
     }                                                                                                \
-    coarse_vcycle_kernel<KK><<<a.nblk, CV_NT, (size_t)bytes, s>>>(a);                                \
-    break;                                                                                           \
+    return spk_launch(coarse_vcycle_kernel<KK>, dim3(a.nblk), dim3(CV_NT), (size_t)bytes, s, a);     \
   }
     SPK_CV(1) SPK_CV(2) SPK_CV(3) SPK_CV(4)
 #undef SPK_CV

@@ -76,6 +76,35 @@ struct SpkApplyArgs {
   int* nan_flag;
 };
 
+// ---- programmatic dependent launch (PDL) ------------------------------------------------------
+// The V-cycle's small-level kernels are each a few microseconds; launched with the PDL attribute a
+// kernel is scheduled while its predecessor in the stream still runs, executes its prologue
+// (shared-memory tables), and waits in spk_pdl_wait() -- before its first global-memory access --
+// until the predecessor has completed and its writes are visible. spk_pdl_trigger() lets the next
+// kernel be scheduled early. Without the attribute both are no-ops.
+__device__ __forceinline__ void spk_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void spk_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool spk_pdl_enabled();     // SPK_PDL=0 disables (api.cu)
+long long spk_pdl_max_ctas();  // launches up to this many CTAs use the attribute (SPK_PDL_MAX)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t spk_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (spk_pdl_enabled() && (long long)grid.x * grid.y * grid.z <= spk_pdl_max_ctas()) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // launchers (stage_apply.cu)
 cudaError_t spk_launch_apply(int K, int Q, bool block_mode, int epi, const SpkApplyArgs& a,
                              cudaStream_t s, int* nctas_out);

@@ -828,6 +828,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{});
     if (t >= 2) xphase(xs + t - 2, IC<p>{});
   };
+  spk_pdl_wait();  // everything above reads parameters / constants only
   load_plane(xs, IC<0>{});
   // unroll the plane loop by two (compile-time buffer offsets); measured on B200 to help every
   // instantiation except the stage-coupled k=2, Q=4 mix (C4's GMRES operator), whose doubled code
@@ -850,6 +851,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     }
   }
 
+  spk_pdl_trigger();  // after the plane pipeline: dependents launch during this grid's tail
   if constexpr (EPI == EPI_DINV) {
     // deterministic per-CTA partial: fixed-shape tree in shared memory
     __syncthreads();
@@ -922,15 +924,6 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
   const int b0 = a.blk_base + (int)blockIdx.y;
   const long long plane_n = (long long)g.ny * g.nz;
   int p0 = 0;
-  if constexpr (STAGED) {
-    const long long i0 = (long long)blockIdx.x * blockDim.x;
-    const long long il = min(i0 + (long long)blockDim.x - 1, g.n - 1);
-    p0 = max((int)(i0 / plane_n) - K, 0);
-    const int p1 = min((int)(il / plane_n) + K, g.nx - 1);
-    const double* src = a.u + (long long)b0 * a.su + (long long)p0 * plane_n;
-    const long long cnt = (long long)(p1 - p0 + 1) * plane_n;
-    for (long long j = tid; j < cnt; j += blockDim.x) ustage[j] = __ldg(src + j);
-  }
   double lamq[1], ith[1];
   lamq[0] = a.lam_uniform ? a.lam[0] : a.lam[b0 - a.blk_base];
   ith[0] = 1.0 / a.c2[b0 - a.blk_base];
@@ -948,6 +941,17 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
     }
   }
   BD::build(bm, bk);
+  spk_pdl_wait();  // the tables above need parameters only (they overlap the previous kernel)
+  spk_pdl_trigger();
+  if constexpr (STAGED) {
+    const long long i0 = (long long)blockIdx.x * blockDim.x;
+    const long long il = min(i0 + (long long)blockDim.x - 1, g.n - 1);
+    p0 = max((int)(i0 / plane_n) - K, 0);
+    const int p1 = min((int)(il / plane_n) + K, g.nx - 1);
+    const double* src = a.u + (long long)b0 * a.su + (long long)p0 * plane_n;
+    const long long cnt = (long long)(p1 - p0 + 1) * plane_n;
+    for (long long j = tid; j < cnt; j += blockDim.x) ustage[j] = __ldg(src + j);
+  }
   __syncthreads();
   double sumsq = 0.0;
   const long long i = (long long)blockIdx.x * blockDim.x + tid;
@@ -1042,11 +1046,9 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
           if (e != cudaSuccess) return e;
           configured_s = true;
         }
-        small_apply_kernel<K, EPI, true><<<grid, 256, stage_bytes, s>>>(a);
-      } else {
-        small_apply_kernel<K, EPI, false><<<grid, 256, 0, s>>>(a);
+        return spk_launch(small_apply_kernel<K, EPI, true>, grid, dim3(256), stage_bytes, s, a);
       }
-      return cudaGetLastError();
+      return spk_launch(small_apply_kernel<K, EPI, false>, grid, dim3(256), 0, s, a);
     }
   }
   const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
@@ -1064,8 +1066,7 @@ cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
   if (((long long)(Q - 1) * a.su + a.g.n) * 8 > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
   dim3 grid(gz, gy, a.nchunks * nb);
   if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
-  kern<<<grid, G::NT, smem, s>>>(a);
-  return cudaGetLastError();
+  return spk_launch(kern, grid, dim3(G::NT), smem, s, a);
 }
 
 #define SPK_EPIS(K, Q, B)                                                   \

@@ -55,6 +55,8 @@ __device__ __forceinline__ void nodediag(const SpkVecArgs& a, int x, int y, int 
 // ---- Chebyshev start: r = b ; x = 0 ; d = c2 * Dinv r   (block or pair Jacobi) ----
 template <int K>
 __global__ void cheb_init_kernel(const __grid_constant__ SpkVecArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const long long n = a.g.n;
   const long long total = (long long)a.nblk * n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -91,6 +93,8 @@ __global__ void cheb_init_kernel(const __grid_constant__ SpkVecArgs a) {
 
 // ---- x += d with a non-finite flag (V-cycle NaN check, multigrid.py:127-128) ----
 __global__ void axpy_flag_kernel(long long total, double* x, const double* d, int* flag) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -143,6 +147,8 @@ __device__ __forceinline__ double transfer_value(const SpkTransferArgs& a, int i
 // output row
 template <int K>
 __global__ void __launch_bounds__(256) transfer_rows_kernel(const __grid_constant__ SpkTransferArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const long long o = (long long)blockIdx.x * 8 + threadIdx.y;
   if (o >= a.outer) return;
   const double* src = a.in + o * (long long)a.nin - a.in_off;
@@ -164,6 +170,8 @@ __global__ void __launch_bounds__(256) transfer_rows_kernel(const __grid_constan
 // (outer row, output node) x bx lanes along the inner index, so no lane idles on a short row
 template <int K>
 __global__ void __launch_bounds__(256) transfer_cols_short_kernel(const __grid_constant__ SpkTransferArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const long long row = (long long)blockIdx.x * blockDim.y + threadIdx.y;  // (o, il) flattened
   const long long in_idx = threadIdx.x;
   if (row >= a.outer * (long long)a.nout || in_idx >= a.inner) return;
@@ -193,6 +201,8 @@ __global__ void __launch_bounds__(256) transfer_cols_short_kernel(const __grid_c
 // outer row), threads along the contiguous inner index -- no index division per element
 template <int K>
 __global__ void __launch_bounds__(256) transfer_cols_kernel(const __grid_constant__ SpkTransferArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const long long in_idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (in_idx >= a.inner) return;
   const int il = a.o_begin + (int)blockIdx.y;
@@ -231,6 +241,8 @@ struct Prolong3 {
 
 template <int K>
 __global__ void __launch_bounds__(256) prolong3d_kernel(const __grid_constant__ SpkTransferArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   using G = Prolong3<K>;
   constexpr int E = G::E, MC = G::MC, MF = G::MF, PS = SPK_KMAX + 1;
   extern __shared__ double sm[];
@@ -344,6 +356,8 @@ struct Restrict3 {
 
 template <int K>
 __global__ void __launch_bounds__(256) restrict3d_kernel(const __grid_constant__ SpkTransferArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   using G = Restrict3<K>;
   constexpr int E = G::E, MC = G::MCR, MF = G::MFR, UNR = 4;
   extern __shared__ double sm[];
@@ -431,6 +445,8 @@ __global__ void __launch_bounds__(256) cheb_rows_kernel(const __grid_constant__ 
     const double dk = ((kx * my) * mz + (mx * ky) * mz) + (mx * my) * kz;
     inv_tab[e] = 1.0 / (a.lam[b] * dm + a.tau * dk);
   }
+  spk_pdl_wait();  // the table above needs parameters only (overlaps the previous kernel)
+  spk_pdl_trigger();
   __syncthreads();
   const unsigned plane = (unsigned)g.ny * (unsigned)g.nz;
   const unsigned n0 = (unsigned)a.row0 * (unsigned)g.nz;
@@ -505,6 +521,8 @@ __global__ void combine_kernel(const __grid_constant__ SpkCombineArgs a) {
 // accumulating
 template <int NIN, int NOUT, bool ACC, bool MASK>
 __global__ void __launch_bounds__(TPB) combine_small_kernel(const __grid_constant__ SpkCombineArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const long long nth = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n; i += 2 * nth) {
     const bool two = i + nth < a.n;
@@ -550,11 +568,11 @@ __global__ void __launch_bounds__(TPB) combine_small_kernel(const __grid_constan
 template <int NIN, int NOUT>
 cudaError_t launch_small(const SpkCombineArgs& a, cudaStream_t s, int nb) {
   if (a.accumulate) {
-    if (a.mask) combine_small_kernel<NIN, NOUT, true, true><<<nb, TPB, 0, s>>>(a);
-    else combine_small_kernel<NIN, NOUT, true, false><<<nb, TPB, 0, s>>>(a);
+    if (a.mask) return spk_launch(combine_small_kernel<NIN, NOUT, true, true>, nb, TPB, 0, s, a);
+    else return spk_launch(combine_small_kernel<NIN, NOUT, true, false>, nb, TPB, 0, s, a);
   } else {
-    if (a.mask) combine_small_kernel<NIN, NOUT, false, true><<<nb, TPB, 0, s>>>(a);
-    else combine_small_kernel<NIN, NOUT, false, false><<<nb, TPB, 0, s>>>(a);
+    if (a.mask) return spk_launch(combine_small_kernel<NIN, NOUT, false, true>, nb, TPB, 0, s, a);
+    else return spk_launch(combine_small_kernel<NIN, NOUT, false, false>, nb, TPB, 0, s, a);
   }
   return cudaGetLastError();
 }
@@ -669,6 +687,8 @@ __device__ __forceinline__ double mgs_body(const SpkMgsArgs& a, double h) {
 }
 
 __global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgsArgs a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   __shared__ double red[TPB];
   const double h = a.v_prev ? *a.h_prev : 0.0;
   double mine;
@@ -679,6 +699,8 @@ __global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgs
 
 // ---- v = w / *h ----
 __global__ void scale_div_kernel(long long n, const double* w, const double* h, double* v) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
   const double d = *h;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -782,18 +804,17 @@ cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s) {
   const long long total = (long long)a.nblk * a.g.n;
   const int nb = grid_for(total);
   switch (K) {
-    case 1: cheb_init_kernel<1><<<nb, TPB, 0, s>>>(a); break;
-    case 2: cheb_init_kernel<2><<<nb, TPB, 0, s>>>(a); break;
-    case 3: cheb_init_kernel<3><<<nb, TPB, 0, s>>>(a); break;
-    case 4: cheb_init_kernel<4><<<nb, TPB, 0, s>>>(a); break;
+    case 1: return spk_launch(cheb_init_kernel<1>, nb, TPB, 0, s, a);
+    case 2: return spk_launch(cheb_init_kernel<2>, nb, TPB, 0, s, a);
+    case 3: return spk_launch(cheb_init_kernel<3>, nb, TPB, 0, s, a);
+    case 4: return spk_launch(cheb_init_kernel<4>, nb, TPB, 0, s, a);
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 cudaError_t spk_launch_axpy_flag(long long total, double* x, const double* d, int* flag, cudaStream_t s) {
-  axpy_flag_kernel<<<grid_for(total), TPB, 0, s>>>(total, x, d, flag);
-  return cudaGetLastError();
+  return spk_launch(axpy_flag_kernel, grid_for(total), TPB, 0, s, total, x, d, flag);
 }
 
 cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cudaStream_t s) {
@@ -818,7 +839,7 @@ cudaError_t spk_launch_prolong3d(int K, int nblk, const SpkTransferArgs& a, cuda
       if (e != cudaSuccess) return e;                                                                 \
       cfg = true;                                                                                     \
     }                                                                                                 \
-    prolong3d_kernel<KK><<<grid, 256, bytes, s>>>(a);                                                 \
+    return spk_launch(prolong3d_kernel<KK>, grid, 256, bytes, s, a);                                  \
     break;                                                                                            \
   }
     SPK_P3(1) SPK_P3(2) SPK_P3(3) SPK_P3(4)
@@ -849,7 +870,7 @@ cudaError_t spk_launch_restrict3d(int K, int nblk, const SpkTransferArgs& a, cud
       if (e != cudaSuccess) return e;                                                                 \
       cfg = true;                                                                                     \
     }                                                                                                 \
-    restrict3d_kernel<KK><<<grid, 256, bytes, s>>>(a);                                                \
+    return spk_launch(restrict3d_kernel<KK>, grid, 256, bytes, s, a);                                 \
     break;                                                                                            \
   }
     SPK_R3(1) SPK_R3(2) SPK_R3(3) SPK_R3(4)
@@ -864,10 +885,10 @@ cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s)
     const unsigned nb = (unsigned)((a.outer + 7) / 8);
     const dim3 blk(32, 8);
     switch (K) {
-      case 1: transfer_rows_kernel<1><<<nb, blk, 0, s>>>(a); break;
-      case 2: transfer_rows_kernel<2><<<nb, blk, 0, s>>>(a); break;
-      case 3: transfer_rows_kernel<3><<<nb, blk, 0, s>>>(a); break;
-      case 4: transfer_rows_kernel<4><<<nb, blk, 0, s>>>(a); break;
+      case 1: return spk_launch(transfer_rows_kernel<1>, nb, blk, 0, s, a);
+      case 2: return spk_launch(transfer_rows_kernel<2>, nb, blk, 0, s, a);
+      case 3: return spk_launch(transfer_rows_kernel<3>, nb, blk, 0, s, a);
+      case 4: return spk_launch(transfer_rows_kernel<4>, nb, blk, 0, s, a);
       default: return cudaErrorInvalidValue;
     }
   } else if (a.inner <= 256) {
@@ -876,20 +897,20 @@ cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s)
     const unsigned nb = (unsigned)((rows + by - 1) / by);
     const dim3 blk(bx, by);
     switch (K) {
-      case 1: transfer_cols_short_kernel<1><<<nb, blk, 0, s>>>(a); break;
-      case 2: transfer_cols_short_kernel<2><<<nb, blk, 0, s>>>(a); break;
-      case 3: transfer_cols_short_kernel<3><<<nb, blk, 0, s>>>(a); break;
-      case 4: transfer_cols_short_kernel<4><<<nb, blk, 0, s>>>(a); break;
+      case 1: return spk_launch(transfer_cols_short_kernel<1>, nb, blk, 0, s, a);
+      case 2: return spk_launch(transfer_cols_short_kernel<2>, nb, blk, 0, s, a);
+      case 3: return spk_launch(transfer_cols_short_kernel<3>, nb, blk, 0, s, a);
+      case 4: return spk_launch(transfer_cols_short_kernel<4>, nb, blk, 0, s, a);
       default: return cudaErrorInvalidValue;
     }
   } else {
     if (a.outer > 65535 || a.nout > 65535) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((a.inner + 255) / 256), (unsigned)a.nout, (unsigned)a.outer);
     switch (K) {
-      case 1: transfer_cols_kernel<1><<<grid, 256, 0, s>>>(a); break;
-      case 2: transfer_cols_kernel<2><<<grid, 256, 0, s>>>(a); break;
-      case 3: transfer_cols_kernel<3><<<grid, 256, 0, s>>>(a); break;
-      case 4: transfer_cols_kernel<4><<<grid, 256, 0, s>>>(a); break;
+      case 1: return spk_launch(transfer_cols_kernel<1>, grid, 256, 0, s, a);
+      case 2: return spk_launch(transfer_cols_kernel<2>, grid, 256, 0, s, a);
+      case 3: return spk_launch(transfer_cols_kernel<3>, grid, 256, 0, s, a);
+      case 4: return spk_launch(transfer_cols_kernel<4>, grid, 256, 0, s, a);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -904,12 +925,12 @@ cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_
   const int nb = (int)nbl;
 #define SPK_ROWS(KK)                                                                   \
   switch (op) {                                                                        \
-    case 0: cheb_rows_kernel<KK, 0><<<nb, 256, 0, s>>>(a); break;                     \
-    case 1: cheb_rows_kernel<KK, 1><<<nb, 256, 0, s>>>(a); break;                     \
-    case 2: cheb_rows_kernel<KK, 2><<<nb, 256, 0, s>>>(a); break;                     \
-    case 3: cheb_rows_kernel<KK, 3><<<nb, 256, 0, s>>>(a); break;                     \
-    case 4: cheb_rows_kernel<KK, 4><<<nb, 256, 0, s>>>(a); break;                     \
-    default: cheb_rows_kernel<KK, 5><<<nb, 256, 0, s>>>(a); break;                    \
+    case 0: return spk_launch(cheb_rows_kernel<KK, 0>, nb, 256, 0, s, a);             \
+    case 1: return spk_launch(cheb_rows_kernel<KK, 1>, nb, 256, 0, s, a);             \
+    case 2: return spk_launch(cheb_rows_kernel<KK, 2>, nb, 256, 0, s, a);             \
+    case 3: return spk_launch(cheb_rows_kernel<KK, 3>, nb, 256, 0, s, a);             \
+    case 4: return spk_launch(cheb_rows_kernel<KK, 4>, nb, 256, 0, s, a);             \
+    default: return spk_launch(cheb_rows_kernel<KK, 5>, nb, 256, 0, s, a);            \
   }
   switch (K) {
     case 1: SPK_ROWS(1) break;
@@ -937,13 +958,11 @@ cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s) {
 int spk_mgs_grid() { return 148 * 8; }
 
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s) {
-  mgs_kernel<<<spk_mgs_grid(), TPB, 0, s>>>(a);
-  return cudaGetLastError();
+  return spk_launch(mgs_kernel, spk_mgs_grid(), TPB, 0, s, a);
 }
 
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s) {
-  scale_div_kernel<<<grid_for(n), TPB, 0, s>>>(n, w, h, v);
-  return cudaGetLastError();
+  return spk_launch(scale_div_kernel, grid_for(n), TPB, 0, s, n, w, h, v);
 }
 
 cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s) {
