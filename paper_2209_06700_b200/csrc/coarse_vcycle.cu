@@ -56,6 +56,7 @@ __device__ __forceinline__ double cv_dinv(int x, int y, int z, int m, double lam
 struct CVShared {
   double* X[SPK_CV_LMAX + 1];
   double* B[SPK_CV_LMAX + 1];
+  double* DI[SPK_CV_LMAX + 1];  // Jacobi inverse diagonal per level (computed once per launch)
   double *R, *D, *W, *T0, *T1, *T2, *T3;
   const double* bm;  // assembled band rows [K+2][2K+1] (reference element, h = 1)
   const double* bk;
@@ -211,11 +212,10 @@ __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int 
   const double* Bv = S.B[l];
   if (!zero_start) cv_apply<K>(S, l, X, S.W, lamp, taup);
   for (int i = threadIdx.x; i < n; i += CV_NT) {
-    const int z = i % m, t = i / m, y = t % m, x = t / m;
     const double r = zero_start ? Bv[i] : Bv[i] - S.W[i];
     if (zero_start) X[i] = 0.0;
     S.R[i] = r;
-    S.D[i] = (cv_dinv<K>(x, y, z, m, lamp, taup) * r) / theta;
+    S.D[i] = (S.DI[l][i] * r) / theta;
   }
   __syncthreads();
   if (a.deg == 1) {
@@ -232,11 +232,10 @@ __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int 
     const bool last = (k == a.deg - 2);
     cv_apply<K>(S, l, S.D, S.W, lamp, taup);
     for (int i = threadIdx.x; i < n; i += CV_NT) {
-      const int z = i % m, t = i / m, y = t % m, x = t / m;
       const double d = S.D[i];
       const double xn = X[i] + d;
       const double r = S.R[i] - S.W[i];
-      const double dn = c1 * d + c2 * (cv_dinv<K>(x, y, z, m, lamp, taup) * r);
+      const double dn = c1 * d + c2 * (S.DI[l][i] * r);
       if (last) {
         const double xf = xn + dn;
         X[i] = xf;
@@ -274,6 +273,10 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
     S.X[l] = p; p += L.n;
     S.B[l] = p; p += L.n;
   }
+  for (int l = 1; l <= lc; ++l) {
+    S.DI[l] = p;
+    p += CVLevel<K>(l).n;
+  }
   S.X[lc] = a.x + (long long)blk * a.sx;
   S.B[lc] = const_cast<double*>(a.b) + (long long)blk * a.sb;
   double* scr = a.scratch + (long long)blk * 3 * nmax;
@@ -286,6 +289,15 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   spk_pdl_wait();
   __syncthreads();
   const double lam = a.lam[blk];
+  for (int l = 1; l <= lc; ++l) {
+    const CVLevel<K> L(l);
+    const double lamp = lam * a.hd[l], taup = a.tau * a.hk[l];
+    for (int i = threadIdx.x; i < L.n; i += CV_NT) {
+      const int z = i % L.m, t = i / L.m, y = t % L.m, x = t / L.m;
+      S.DI[l][i] = cv_dinv<K>(x, y, z, L.m, lamp, taup);
+    }
+  }
+  __syncthreads();
   bool bad[SPK_CV_LMAX + 1];
 #pragma unroll
   for (int l = 0; l <= SPK_CV_LMAX; ++l) bad[l] = false;
@@ -330,6 +342,10 @@ long long spk_coarse_vcycle_smem(int K, int lc) {
   for (int l = 0; l < lc; ++l) {
     const long long m = ((long long)K << l) + 1;
     tot += 2 * m * m * m;
+  }
+  for (int l = 1; l <= lc; ++l) {  // Jacobi tables
+    const long long m = ((long long)K << l) + 1;
+    tot += m * m * m;
   }
   const long long m = ((long long)K << lc) + 1;
   return (tot + 4 * m * m * m) * (long long)sizeof(double);
