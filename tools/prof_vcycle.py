@@ -12,6 +12,8 @@ from paper_2209_06700_b200.multigrid import MultiBlockSolver, VCycleConfig
 k = int(os.environ.get("K", 2)); L = int(os.environ.get("L", 7)); nb = int(os.environ.get("NB", 4))
 deg = int(os.environ.get("DEG", 3))
 h = build_hierarchy(3, L, k)
+if "TARGET" in os.environ:  # K1 x-chunking target (CTAs per launch; 0 = automatic)
+    _lib.load().spk_set_chunks(h.ctx, int(os.environ["TARGET"]))
 if "SPLIT" in os.environ:  # Chebyshev split threshold (block-DoFs); 0 = always split
     _lib.call("spk_set_cheb_split", h.ctx, int(os.environ["SPLIT"]))
 n = h.levels[L].n_dofs
