@@ -24,6 +24,8 @@ struct spk_ctx {
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
+  int mgs_coop = 1;                  // cooperative single-launch MGS column for small vectors (SPK_MGS_COOP)
+  long long mgs_coop_max = 1LL << 22; // ... up to this many doubles
   long long cv_max_nodes = 2200;  // fused coarse V-cycle: top level up to this many nodes (SPK_CV_MAXN;
                                   // measured: a single CTA loses at 17^3 nodes, k=2 C3 V-cycle 479 vs 569 us)
   long long fuse_restrict_max = 1LL << 22;  // fused 3D restriction up to nblk * n fine DoFs (SPK_FUSE_RESTRICT_MAX)
@@ -356,6 +358,8 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (const char* e = std::getenv("SPK_FUSE_TRANSFER")) c->fuse_transfer = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_RESTRICT_MAX")) c->fuse_restrict_max = std::atoll(e);
   if (const char* e = std::getenv("SPK_CV_MAXN")) c->cv_max_nodes = std::atoll(e);
+  if (const char* e = std::getenv("SPK_MGS_COOP")) c->mgs_coop = std::atoi(e);
+  if (const char* e = std::getenv("SPK_MGS_COOP_MAX")) c->mgs_coop_max = std::atoll(e);
   c->dim = dim;
   c->max_level = max_level;
   c->K = degree;
@@ -972,6 +976,17 @@ int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, d
   // v_{j+1} = w / h_{j+1,j}; hcol points at H[0, j] (H[i, j] = hcol[i], device-resident)
   if (!c) return fail(SPK_ECONFIG, "null context");
   if (j < 0 || !basis || !w || !hcol) return fail(SPK_ECONFIG, "mgs_column: bad arguments");
+  // small vectors: the whole column in one cooperative launch (the j+2 launches are latency-bound)
+  if (c->mgs_coop && n <= c->mgs_coop_max && j + 1 < SPK_MGS_MAXCOL) {
+    if (int rc = ensure_scratch(c, 2 * spk_mgs_coop_grid())) return rc;
+    SpkMgsColArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.n = n; a.j = j; a.w = w; a.hcol = hcol; a.v_next = v_next; a.partial = c->partial;
+    for (int i = 0; i <= j; ++i) a.basis[i] = basis[i];
+    cudaError_t e = spk_launch_mgs_column_coop(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mgs_column_coop");
+    return SPK_OK;
+  }
   int rc = spk_mgs(c, n, w, nullptr, nullptr, basis[0], hcol, stream);
   for (int i = 1; rc == SPK_OK && i <= j; ++i) rc = spk_mgs(c, n, w, basis[i - 1], hcol + i - 1, basis[i], hcol + i, stream);
   if (rc == SPK_OK) rc = spk_mgs(c, n, w, basis[j], hcol + j, nullptr, hcol + j + 1, stream);

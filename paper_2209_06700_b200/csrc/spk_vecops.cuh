@@ -52,6 +52,17 @@ struct SpkTransferArgs {
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];
 };
 
+#define SPK_MGS_MAXCOL 240
+struct SpkMgsColArgs {  // one MGS column (spk_mgs_column) in one cooperative launch
+  long long n;
+  int j;
+  double* w;
+  double* hcol;     // H[0 .. j+1, j]
+  double* v_next;   // w / H[j+1, j] (optional)
+  double* partial;  // 2 * grid doubles
+  const double* basis[SPK_MGS_MAXCOL];
+};
+
 struct SpkCombineArgs {
   const double* in[SPK_CMAX];  // input rows (local rows, or rows in peer GPUs' memory)
   double* out;
@@ -118,6 +129,8 @@ cudaError_t spk_launch_restrict3d(int K, int nblk, const SpkTransferArgs& a, cud
 cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s);
 int spk_mgs_grid();
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
+int spk_mgs_coop_grid();
+cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s);
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s);
 cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s);
 cudaError_t spk_launch_lincomb(long long n, int k, const double* const* vs, const double* y, double* z,

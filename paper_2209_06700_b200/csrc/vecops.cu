@@ -6,10 +6,13 @@
 //     (krylov.py:74-82), device-resident Hessenberg entries (no host round trip per dot)
 //   * RHS assembly for separable sources and nodal interpolation (fem.py:220-246, :368-372)
 #include <cmath>
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "spk_internal.cuh"
 #include "spk_vecops.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -697,6 +700,40 @@ __global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgs
   finalize_partials(block_sum(mine, red), a.partial, a.counter, a.out, a.v_cur == nullptr, red);
 }
 
+// ---- one MGS column in one cooperative launch (small vectors: each of the j+2 separate launches is
+//      latency-bound there). Same sweeps (mgs_body); the per-CTA partials are summed by every CTA in
+//      CTA order after a grid barrier (run-to-run deterministic); partials double-buffered by step.
+__global__ void __launch_bounds__(TPB) mgs_column_coop_kernel(const __grid_constant__ SpkMgsColArgs c) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[TPB];
+  SpkMgsArgs a;
+  a.n = c.n;
+  a.w = c.w;
+  double hprev = 0.0;
+  for (int i = 0; i <= c.j + 1; ++i) {
+    a.v_prev = i > 0 ? c.basis[i - 1] : nullptr;
+    a.v_cur = i <= c.j ? c.basis[i] : nullptr;
+    double mine;
+    if (a.v_prev) mine = a.v_cur ? mgs_body<true, true>(a, hprev) : mgs_body<true, false>(a, hprev);
+    else mine = a.v_cur ? mgs_body<false, true>(a, hprev) : mgs_body<false, false>(a, hprev);
+    const double bs = block_sum(mine, red);
+    double* part = c.partial + (i & 1) * gridDim.x;
+    if (threadIdx.x == 0) part[blockIdx.x] = bs;
+    grid.sync();
+    double sp = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) sp += part[b];
+    const double tot = block_sum(sp, red);
+    __syncthreads();  // every thread has read red[0] before the next block_sum reuses it
+    hprev = (i == c.j + 1) ? sqrt(tot) : tot;
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.hcol[i] = hprev;
+  }
+  if (c.v_next) {  // v_{j+1} = w / h_{j+1,j} (w complete: the last step ended with a grid barrier)
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < c.n;
+         k += (long long)gridDim.x * blockDim.x)
+      c.v_next[k] = c.w[k] / hprev;
+  }
+}
+
 // ---- v = w / *h ----
 __global__ void scale_div_kernel(long long n, const double* w, const double* h, double* v) {
   spk_pdl_wait();
@@ -959,6 +996,27 @@ int spk_mgs_grid() { return 148 * 8; }
 
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s) {
   return spk_launch(mgs_kernel, spk_mgs_grid(), TPB, 0, s, a);
+}
+
+int spk_mgs_coop_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_column_coop_kernel, TPB, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = sms * (per_sm < 4 ? per_sm : 4);
+  }
+  return g;
+}
+
+cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s) {
+  void* args[] = {const_cast<SpkMgsColArgs*>(&a)};
+  return cudaLaunchCooperativeKernel((const void*)mgs_column_coop_kernel, dim3(spk_mgs_coop_grid()), dim3(TPB),
+                                     args, 0, s);
 }
 
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s) {
