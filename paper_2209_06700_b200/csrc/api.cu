@@ -25,7 +25,7 @@ struct spk_ctx {
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
   int mgs_coop = 1;                  // cooperative single-launch MGS column for small vectors (SPK_MGS_COOP)
-  long long mgs_coop_max = 1LL << 22; // ... up to this many doubles
+  long long mgs_coop_max = 1LL << 25; // ... up to this many doubles (measured: C5 -5 %, C4 at 68M neutral)
   long long cv_max_nodes = 2200;  // fused coarse V-cycle: top level up to this many nodes (SPK_CV_MAXN;
                                   // measured: a single CTA loses at 17^3 nodes, k=2 C3 V-cycle 479 vs 569 us)
   long long fuse_restrict_max = 1LL << 22;  // fused 3D restriction up to nblk * n fine DoFs (SPK_FUSE_RESTRICT_MAX)
