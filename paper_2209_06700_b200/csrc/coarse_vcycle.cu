@@ -57,6 +57,7 @@ struct CVShared {
   double* X[SPK_CV_LMAX + 1];
   double* B[SPK_CV_LMAX + 1];
   double* DI[SPK_CV_LMAX + 1];  // Jacobi inverse diagonal per level (computed once per launch)
+  const int* CO[SPK_CV_LMAX + 1];  // packed node coordinates x | y << 10 | z << 20 per level (no div/mod)
   double *R, *D, *W, *T0, *T1, *T2, *T3;
   const double* bm;  // assembled band rows [K+2][2K+1] (reference element, h = 1)
   const double* bk;
@@ -68,8 +69,9 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
   constexpr int W = 2 * K + 1;
   const CVLevel<K> L(l);
   const int m = L.m, n = L.n, mm = m * m;
+  const int* co = S.CO[l];
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // z: T0 = Mz u, T1 = Kz u
-    const int z = i % m, t = i / m, y = t % m, x = t / m;
+    const int cw = co[i], x = cw & 1023, y = (cw >> 10) & 1023, z = cw >> 20;
     const int c = cv_cls<K>(z, m);
     double a = 0.0, b = 0.0;
 #pragma unroll
@@ -85,7 +87,7 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // y: ma = My a, c = Ky a + My b -> p, q
-    const int t = i / m, y = t % m;
+    const int y = (co[i] >> 10) & 1023;
     const int c = cv_cls<K>(y, m);
     double ma = 0.0, cc = 0.0;
 #pragma unroll
@@ -102,7 +104,7 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // x: v = Mx p + Kx q ; boundary rows identity
-    const int z = i % m, t = i / m, y = t % m, x = t / m;
+    const int cw = co[i], x = cw & 1023, y = (cw >> 10) & 1023, z = cw >> 20;
     if (cv_bnd(x, y, z, m)) {
       v[i] = u[i];
       continue;
@@ -277,6 +279,18 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
     S.DI[l] = p;
     p += CVLevel<K>(l).n;
   }
+  {
+    int* ip = reinterpret_cast<int*>(p);
+    for (int l = 0; l <= lc; ++l) {
+      const CVLevel<K> L(l);
+      for (int i = threadIdx.x; i < L.n; i += CV_NT) {
+        const int z = i % L.m, t = i / L.m, y = t % L.m, x = t / L.m;
+        ip[i] = x | (y << 10) | (z << 20);
+      }
+      S.CO[l] = ip;
+      ip += L.n;
+    }
+  }
   S.X[lc] = a.x + (long long)blk * a.sx;
   S.B[lc] = const_cast<double*>(a.b) + (long long)blk * a.sb;
   double* scr = a.scratch + (long long)blk * 3 * nmax;
@@ -347,6 +361,12 @@ long long spk_coarse_vcycle_smem(int K, int lc) {
     const long long m = ((long long)K << l) + 1;
     tot += m * m * m;
   }
+  long long ints = 0;
+  for (int l = 0; l <= lc; ++l) {  // coordinate tables
+    const long long m = ((long long)K << l) + 1;
+    ints += m * m * m;
+  }
+  tot += (ints + 1) / 2;
   const long long m = ((long long)K << lc) + 1;
   return (tot + 4 * m * m * m) * (long long)sizeof(double);
 }
