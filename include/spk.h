@@ -21,6 +21,7 @@
  *   spk_transfer            prolong / restrict (+ mask, + accumulate)     fem.py:189-211, multigrid.py:171-177
  *   spk_combine             SPEC tensor_ops dense_combine (D (x) I) u
  *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
+ *   spk_mgs_partial / spk_sqrt_dev        gmres MGS with all-reduced dots   krylov.py:74-82 (+ PAPER.md:426-443)
  *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
  *   spk_mask                GridHierarchy.constrain                       fem.py:153-158
  *   spk_peer_combine        SPEC tensor_ops sharedmem_combine (D (x) I) u
@@ -114,7 +115,6 @@ int spk_combine(spk_ctx* ctx, int mask_level, long long n, int nin, int nout, co
                 const double* in, long long sin, double* out, long long sout, int accumulate,
                 void* stream);
 
-/* GMRES: w -= (*h_prev) v_prev ; *out = <v_cur, w>  (v_cur == NULL: *out = ||w||) */
 /* out_o = sum_j D[o, j] in_rows[j] over n entries; in_rows is a HOST array of nin device pointers,
  * which may point into peer GPUs' memory (CUDA IPC windows): the stage exchange and the combine
  * arithmetic are one kernel reading over NVLink (the shared-memory combine backend) */
@@ -141,6 +141,7 @@ int spk_set_vsplit(spk_ctx* ctx, int on);
 int spk_set_cheb_split(spk_ctx* ctx, long long min_block_dofs);
 /* 1 if the Chebyshev steps of this level run split (K1 STORE + pointwise update), 0 if fused */
 int spk_cheb_split(spk_ctx* ctx, int level, int nblk);
+/* GMRES: w -= (*h_prev) v_prev ; *out = <v_cur, w>  (v_cur == NULL: *out = ||w||) */
 int spk_mgs(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
             const double* v_cur, double* out, void* stream);
 int spk_scale_div(long long n, const double* w, const double* h, double* v, void* stream);
@@ -154,6 +155,12 @@ int spk_coarse_vcycle_level(spk_ctx* ctx);
 int spk_coarse_vcycle(spk_ctx* ctx, int lc, int nblk, const double* lams, double tau, int deg,
                       const double* coef, const double* cinv, const double* b, double* x, double* scratch,
                       int* flags, void* stream);
+/* distributed MGS (krylov.py:74-82 with all-reduced inner products): same sweep as spk_mgs, but
+ * with v_cur == NULL *out is this rank's sum of squares (the caller all-reduces it, then
+ * spk_sqrt_dev turns the sum into the norm H[j+1, j]) */
+int spk_mgs_partial(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
+                    const double* v_cur, double* out, void* stream);
+int spk_sqrt_dev(double* x, int count, void* stream);
 /* One MGS column (krylov.py:74-82) in one call: the j+2 fused spk_mgs sweeps of w against basis[0..j]
  * (host array of device pointers), H[0..j+1, j] written to hcol (device), then v_next = w / H[j+1, j]
  * when v_next is not NULL. Same launches and order as the per-sweep calls. */

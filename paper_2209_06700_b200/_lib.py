@@ -70,6 +70,8 @@ _SIGS = {
     "spk_ipc_free": ([c_vp], c_int),
     "spk_copy_d2d": ([c_vp, c_vp, c_ll, c_vp], c_int),
     "spk_mgs": ([c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "spk_mgs_partial": ([c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "spk_sqrt_dev": ([c_vp, c_int, c_vp], c_int),
     "spk_scale_div": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_mgs_column": ([c_vp, c_ll, c_int, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_coarse_vcycle_level": ([c_vp], c_int),

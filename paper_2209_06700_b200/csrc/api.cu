@@ -132,7 +132,11 @@ int check_level(const spk_ctx* c, int level) {
 
 int ensure_scratch(spk_ctx* c, int need) {
   if (c->partial_cap >= need && c->counter) return SPK_OK;
-  if (c->partial) cudaFree(c->partial);
+  if (c->partial) {
+    cudaFree(c->partial);
+    c->partial = nullptr;  // never leave a dangling buffer behind a failed cudaMalloc below
+    c->partial_cap = 0;
+  }
   if (!c->counter) {
     cudaError_t e = cudaMalloc(&c->counter, 64 * sizeof(unsigned));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counter)");
@@ -932,9 +936,28 @@ int spk_mgs(spk_ctx* c, long long n, double* w, const double* v_prev, const doub
   if (int rc = ensure_scratch(c, spk_mgs_grid())) return rc;
   SpkMgsArgs a;
   a.n = n; a.w = w; a.v_prev = v_prev; a.h_prev = h_prev; a.v_cur = v_cur; a.out = out;
-  a.partial = c->partial; a.counter = c->counter;
+  a.partial = c->partial; a.counter = c->counter; a.sq = 0;
   cudaError_t e = spk_launch_mgs(a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "mgs");
+  return SPK_OK;
+}
+
+int spk_mgs_partial(spk_ctx* c, long long n, double* w, const double* v_prev, const double* h_prev,
+                    const double* v_cur, double* out, void* stream) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (int rc = ensure_scratch(c, spk_mgs_grid())) return rc;
+  SpkMgsArgs a;
+  a.n = n; a.w = w; a.v_prev = v_prev; a.h_prev = h_prev; a.v_cur = v_cur; a.out = out;
+  a.partial = c->partial; a.counter = c->counter; a.sq = 1;
+  cudaError_t e = spk_launch_mgs(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mgs_partial");
+  return SPK_OK;
+}
+
+int spk_sqrt_dev(double* x, int count, void* stream) {
+  if (count < 0 || count > 32) return fail(SPK_ECONFIG, "sqrt_dev: count must lie in [0, 32]");
+  cudaError_t e = spk_launch_sqrt(x, count, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sqrt");
   return SPK_OK;
 }
 

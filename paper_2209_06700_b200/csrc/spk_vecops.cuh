@@ -81,6 +81,7 @@ struct SpkMgsArgs {
   double* out;
   double* partial;
   unsigned* counter;
+  int sq;  // v_cur == null: 1 -> *out = sum w^2 (a rank's partial, all-reduced by the caller), 0 -> ||w||
 };
 
 struct SpkSepArgs {
@@ -131,6 +132,7 @@ int spk_mgs_grid();
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
 int spk_mgs_coop_grid();
 cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s);
+cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s);
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s);
 cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s);
 cudaError_t spk_launch_lincomb(long long n, int k, const double* const* vs, const double* y, double* z,

@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgs
   double mine;
   if (a.v_prev) mine = a.v_cur ? mgs_body<true, true>(a, h) : mgs_body<true, false>(a, h);
   else mine = a.v_cur ? mgs_body<false, true>(a, h) : mgs_body<false, false>(a, h);
-  finalize_partials(block_sum(mine, red), a.partial, a.counter, a.out, a.v_cur == nullptr, red);
+  finalize_partials(block_sum(mine, red), a.partial, a.counter, a.out, a.v_cur == nullptr && !a.sq, red);
 }
 
 // ---- one MGS column in one cooperative launch (small vectors: each of the j+2 separate launches is
@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(TPB) mgs_column_coop_kernel(const __grid_const
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[TPB];
   SpkMgsArgs a;
+  a.sq = 0;
   a.n = c.n;
   a.w = c.w;
   double hprev = 0.0;
@@ -742,6 +743,11 @@ __global__ void scale_div_kernel(long long n, const double* w, const double* h, 
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     v[i] = w[i] / d;
+}
+
+// ---- x <- sqrt(x) for a few device scalars (distributed GMRES: all-reduced sum of squares -> norm) ----
+__global__ void sqrt_kernel(double* x, int count) {
+  if (threadIdx.x < count) x[threadIdx.x] = sqrt(x[threadIdx.x]);
 }
 
 // ---- sum of a per-CTA partial vector on device (power iteration norm) ----
@@ -1017,6 +1023,11 @@ cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s) {
   void* args[] = {const_cast<SpkMgsColArgs*>(&a)};
   return cudaLaunchCooperativeKernel((const void*)mgs_column_coop_kernel, dim3(spk_mgs_coop_grid()), dim3(TPB),
                                      args, 0, s);
+}
+
+cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s) {
+  sqrt_kernel<<<1, 32, 0, s>>>(x, count);
+  return cudaGetLastError();
 }
 
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s) {

@@ -21,54 +21,99 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .errors import NumericalFailureError
 from .runtime import Counters, RankGrid, all_reduce_sum, host_staged, stage_groups  # noqa: F401
 from .tableau import crout_lu, radau_iia, spectral_real
 
 
+def _combine_into(out, D, rows, accumulate):
+    """out (+)= D @ rows: the device kernel (spk_combine, K7) for CUDA tensors, torch for the CPU
+    test doubles."""
+    if out.is_cuda:
+        from . import _lib
+        from ._device import stream_ptr
+        Dc = np.ascontiguousarray(D, dtype=np.float64)
+        _lib.call("spk_combine", None, -1, out.shape[-1], Dc.shape[1], Dc.shape[0], Dc.ctypes.data_as(_lib.P_dbl),
+                  rows.data_ptr(), rows.stride(0), out.data_ptr(), out.stride(0), 1 if accumulate else 0,
+                  stream_ptr(out.device))
+        return
+    blk = torch.from_numpy(np.ascontiguousarray(D)).to(out.dtype)
+    if accumulate:
+        out.addmm_(blk, rows)
+    else:
+        torch.mm(blk, rows, out=out)
+
+
 class RingCombiner:
-    """v_own = sum_j D[own, j] x_j with x distributed by stage groups (Cannon-like rotation).
+    """v_own = sum_j D[own, j] x_j with x distributed by stage groups (Cannon-like rotation,
+    PAPER.md:481-548; SPEC tensor_ops rotate_combine).
 
     `rank` is the position in the ring (the stage group index), `world` the ring length; `ranks`
-    maps ring positions to global ranks (default: identity, the default group)."""
+    maps ring positions to global ranks (default: identity, the default group).
+
+    Double-buffered: in round s the transfer of the held stage group to the left neighbour (and the
+    receive of the next one from the right) is posted BEFORE round s's combine kernel is queued, so
+    on NCCL the NVLink transfer of round s+1's operand overlaps round s's FMA; the received buffer is
+    only read after the request completes. Two persistent wire buffers per shape, no per-round
+    allocation or zero-fill. Groups may be uneven or empty (Q not a multiple of the ring length)."""
 
     def __init__(self, groups, rank, world, group=None, ranks=None, counters=None):
         self.groups, self.rank, self.world, self.group = groups, rank, world, group
         self.ranks = list(ranks) if ranks is not None else list(range(world))
         self.counters = counters if counters is not None else Counters()
         self.shift_rounds = 0
+        self._wires = {}
+
+    def _buffers(self, rows, n, dtype, device):
+        key = (rows, n, dtype, str(device))
+        if key not in self._wires:
+            self._wires[key] = [torch.zeros((rows, n), dtype=dtype, device=device) for _ in range(2)]
+        return self._wires[key]
 
     def __call__(self, D, x_local, in_groups=None, out_groups=None):
         """in_groups / out_groups: row ranges of D's columns / rows owned by each rank (default:
         the stage groups for both)."""
-        D = np.asarray(D)
+        D = np.asarray(D, dtype=np.float64)
         ig = in_groups or self.groups
         og = out_groups or self.groups
         r, W = self.rank, self.world
         lo, hi = og[r]
         n = x_local.shape[-1]
-        out = torch.zeros((hi - lo, n), dtype=x_local.dtype, device=x_local.device)
-        held = x_local.contiguous()
-        held_owner = r
+        dev = x_local.device
+        out = torch.zeros((hi - lo, n), dtype=x_local.dtype, device=dev)
         maxg = max(max(g[1] - g[0] for g in ig), 1)
+        ilo, ihi = ig[r]
+        if W == 1:
+            if hi > lo and ihi > ilo:
+                _combine_into(out, D[lo:hi, ilo:ihi], x_local[: ihi - ilo].contiguous(), False)
+            return out
+        # gloo moves host memory only: stage the wire buffers on the host for CUDA tensors
+        host = x_local.is_cuda and dist.get_backend(self.group) == "gloo"
+        cur, nxt = self._buffers(maxg, n, x_local.dtype, "cpu" if host else dev)
+        if ihi > ilo:
+            cur[: ihi - ilo].copy_(x_local[: ihi - ilo])
+        held_owner = r
+        first = True
         for s in range(W):
-            hlo, hhi = ig[held_owner]
-            blk = torch.from_numpy(np.ascontiguousarray(D[lo:hi, hlo:hhi])).to(x_local.device, x_local.dtype)
-            if hhi > hlo and hi > lo:
-                out.addmm_(blk, held[: hhi - hlo])
-            if s < W - 1:
-                send = torch.zeros((maxg, n), dtype=x_local.dtype, device=x_local.device)
-                send[: held.shape[0]] = held[: hhi - hlo]
-                wire = host_staged(send, self.group)
-                recv = torch.empty_like(wire)
-                ops = [dist.P2POp(dist.isend, wire, self.groups_rank((r - 1) % W), self.group),
-                       dist.P2POp(dist.irecv, recv, self.groups_rank((r + 1) % W), self.group)]
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
-                held = recv.to(x_local.device)
-                held_owner = (held_owner + 1) % W
+            reqs = []
+            if s < W - 1:  # post round s+1's exchange before round s's combine
+                ops = [dist.P2POp(dist.isend, cur, self.groups_rank((r - 1) % W), self.group),
+                       dist.P2POp(dist.irecv, nxt, self.groups_rank((r + 1) % W), self.group)]
+                reqs = dist.batch_isend_irecv(ops)
                 self.shift_rounds += 1
                 self.counters.shift_rounds += 1
-                self.counters.add_send(wire)
+                self.counters.add_send(cur)
+            hlo, hhi = ig[held_owner]
+            if hhi > hlo and hi > lo:
+                rows = cur[: hhi - hlo]
+                if host:
+                    rows = rows.to(dev)
+                _combine_into(out, D[lo:hi, hlo:hhi], rows, not first)
+                first = False
+            for req in reqs:
+                req.wait()
+            cur, nxt = nxt, cur
+            held_owner = (held_owner + 1) % W
         return out
 
     def groups_rank(self, r):
@@ -193,19 +238,39 @@ class PeerCombiner:
 class DistKrylov:
     """Right-preconditioned MGS GMRES (krylov.py:28-103 semantics) with all-reduced inner products.
 
-    `owned(v)` selects the entries a rank owns (slab halos excluded from the dots)."""
+    `owned(v)` selects the entries a rank owns (slab halos excluded from the dots).
 
-    def __init__(self, group=None, owned=None, counters=None):
+    Device path (CUDA vectors, every entry owned): each MGS sweep is one fused `spk_mgs_partial`
+    launch (w -= h_prev v_prev; local <v_cur, w>) writing this rank's partial straight into the
+    device Hessenberg slot, which is then all-reduced in place (NCCL: 8 bytes on the stream, no host
+    sync); the next sweep reads the reduced h from device memory. The norm slot is all-reduced as a
+    sum of squares and square-rooted on device. The host sees ONE copy per iteration: the finished
+    column for the least-squares solve (np.linalg.lstsq as in krylov.py:106-110). Slab partitions
+    (halo entries excluded) compute the partials with torch on device, same order, still without a
+    host sync per dot. CPU tensors (gloo tests) take the host path."""
+
+    def __init__(self, group=None, owned=None, counters=None, ctx=None):
         self.group = group
-        self.owned = owned or (lambda v: v)
+        self.owned = owned
         self.counters = counters
+        self.ctx = ctx
+
+    def _own(self, v):
+        return self.owned(v) if self.owned is not None else v
 
     def dot(self, a, b):
-        t = torch.sum(self.owned(a) * self.owned(b)).reshape(1).to(torch.float64)
+        t = torch.sum(self._own(a) * self._own(b)).reshape(1).to(torch.float64)
         all_reduce_sum(t, self.group, self.counters)
         return float(t.item())
 
+    def _lstsq(self, H, g, k):
+        y, *_ = np.linalg.lstsq(H[: k + 1, :k], g[: k + 1], rcond=None)
+        res = float(np.linalg.norm(g[: k + 1] - H[: k + 1, :k] @ y))
+        return y, res
+
     def solve(self, A, P, b, rel_tol=1e-12, max_iter=200):
+        if b.is_cuda:
+            return self._solve_device(A, P, b, rel_tol, max_iter)
         beta = np.sqrt(self.dot(b, b))
         hist = [beta]
         if beta == 0.0:
@@ -223,24 +288,100 @@ class DistKrylov:
                 w = w - H[i, j] * V[i]
             H[j + 1, j] = np.sqrt(self.dot(w, w))
             if not np.all(np.isfinite(H[: j + 2, j])):
-                raise FloatingPointError("non-finite GMRES value")
+                raise NumericalFailureError("non-finite value in distributed GMRES")
             k = j + 1
             if abs(H[j + 1, j]) < 1e-30:
                 happy = True
             else:
                 V.append(w / H[j + 1, j])
-            y, *_ = np.linalg.lstsq(H[: k + 1, :k], g[: k + 1], rcond=None)
-            res = float(np.linalg.norm(g[: k + 1] - H[: k + 1, :k] @ y))
+            y, res = self._lstsq(H, g, k)
             hist.append(res)
             if happy or res <= target:
                 break
-        y, *_ = np.linalg.lstsq(H[: k + 1, :k], g[: k + 1], rcond=None)
+        y, _ = self._lstsq(H, g, k)
         z = torch.zeros_like(b)
         for i in range(k):
             z = z + float(y[i]) * V[i]
         x = P(z)
         r = b - A(x)
         true_res = np.sqrt(self.dot(r, r))
+        conv = happy or true_res <= target * (1 + 1e-9) or hist[-1] <= target
+        return x, k, hist, conv
+
+    # ---- device path ----
+    def _sweep(self, Hd, w, v_prev, hp, v_cur, out):
+        """Hd[out] = local <v_cur, w - Hd[hp] v_prev> (or local sum w^2 if v_cur is None); w updated."""
+        if self.owned is None:
+            from . import _lib
+            from ._device import stream_ptr
+            _lib.call("spk_mgs_partial", self.ctx, w.numel(), w.data_ptr(),
+                      v_prev.data_ptr() if v_prev is not None else None,
+                      Hd[hp:].data_ptr() if v_prev is not None else None,
+                      v_cur.data_ptr() if v_cur is not None else None, Hd[out:].data_ptr(), stream_ptr(w.device))
+            return
+        if v_prev is not None:
+            w.sub_(Hd[hp] * v_prev)
+        wo = self._own(w)
+        c = self._own(v_cur) if v_cur is not None else wo
+        torch.sum(c * wo, out=Hd[out])
+
+    def _solve_device(self, A, P, b, rel_tol, max_iter):
+        if self.owned is None and self.ctx is None:
+            from .krylov import _ctx
+            self.ctx = _ctx()
+        b = b.contiguous()
+        Hd = torch.zeros((max_iter + 2) * (max_iter + 2), dtype=torch.float64, device=b.device)
+        cols = max_iter + 2
+        # beta = ||b||: sum of squares, all-reduced, square-rooted on device
+        nb = (max_iter + 1) * cols
+        self._sweep(Hd, b, None, 0, None, nb)
+        all_reduce_sum(Hd[nb : nb + 1], self.group, self.counters)
+        from . import _lib
+        from ._device import stream_ptr
+        st = stream_ptr(b.device)
+        _lib.call("spk_sqrt_dev", Hd[nb:].data_ptr(), 1, st)
+        beta = float(Hd[nb].item())
+        hist = [beta]
+        if beta == 0.0:
+            return torch.zeros_like(b), 0, hist, True
+        target = rel_tol * beta
+        V = [b / Hd[nb]]
+        H = np.zeros((max_iter + 1, max_iter))
+        g = np.zeros(max_iter + 1)
+        g[0] = beta
+        k, happy = 0, False
+        for j in range(max_iter):
+            w = A(P(V[j])).contiguous().clone()
+            c0 = j * cols
+            for i in range(j + 1):
+                self._sweep(Hd, w, V[i - 1] if i > 0 else None, c0 + i - 1, V[i], c0 + i)
+                all_reduce_sum(Hd[c0 + i : c0 + i + 1], self.group, self.counters)
+            self._sweep(Hd, w, V[j], c0 + j, None, c0 + j + 1)
+            all_reduce_sum(Hd[c0 + j + 1 : c0 + j + 2], self.group, self.counters)
+            _lib.call("spk_sqrt_dev", Hd[c0 + j + 1 :].data_ptr(), 1, st)
+            col = Hd[c0 : c0 + j + 2].cpu().numpy()   # the one host copy of the iteration
+            if not np.all(np.isfinite(col)):
+                raise NumericalFailureError("non-finite value in distributed GMRES")
+            H[: j + 2, j] = col
+            k = j + 1
+            if abs(H[j + 1, j]) < 1e-30:
+                happy = True
+            else:
+                V.append(w / Hd[c0 + j + 1])
+            y, res = self._lstsq(H, g, k)
+            hist.append(res)
+            if happy or res <= target:
+                break
+        y, _ = self._lstsq(H, g, k)
+        z = torch.zeros_like(b)
+        for i in range(k):
+            z.add_(V[i], alpha=float(y[i]))
+        x = P(z)
+        r = b - A(x)
+        nr = (max_iter + 1) * cols + 1
+        self._sweep(Hd, r, None, 0, None, nr)
+        all_reduce_sum(Hd[nr : nr + 1], self.group, self.counters)
+        true_res = float(np.sqrt(Hd[nr].item()))
         conv = happy or true_res <= target * (1 + 1e-9) or hist[-1] <= target
         return x, k, hist, conv
 
@@ -267,6 +408,10 @@ class StageParallelStepper:
             raise ValueError(f"rank {rank} is idle in the {self.grid.topology} grid")
         self.s_idx, self.b_idx = sb
         S = self.grid.S
+        if S > 1 and self.grid.B > 1:
+            # the row groups carry the stage combines and the update all-reduce; without them those
+            # would run on the world group and silently add different x-slabs together
+            self.grid.init_groups()
         self.groups = stage_groups(Q, S)
         self.lo, self.hi = self.groups[self.s_idx]
         row_group = self.grid.row_group(self.b_idx) if self.grid.B > 1 else group
@@ -280,7 +425,8 @@ class StageParallelStepper:
                                      device=getattr(getattr(backend, "h", None), "device", None))
         else:
             raise ValueError(f"unknown combine backend {combine!r}")
-        self.kry = DistKrylov(group, owned=getattr(backend, "owned", None), counters=self.grid.counters)
+        self.kry = DistKrylov(group, owned=getattr(backend, "owned", None), counters=self.grid.counters,
+                              ctx=getattr(getattr(backend, "h", None), "ctx", None))
         backend.setup(self.lams[self.lo : self.hi], self.tau)
 
     def A_op(self, k):
@@ -430,7 +576,8 @@ class DirectComplexParallelStepper:
         kst = self.ring(self.Wb, z, in_groups=self.row_groups, out_groups=self.groups)
         part = self.tau * torch.einsum("i,in->n", torch.as_tensor(self.b[self.lo : self.hi], dtype=kst.dtype,
                                                                   device=kst.device), kst)
-        dist.all_reduce(part, group=self.group)
+        if self.world > 1:
+            all_reduce_sum(part, self.group)
         return u_n + part, its
 
 

@@ -251,3 +251,74 @@ def test_direct_complex_parallel_matches_oracle(Q, variant):
     for i in range(2):
         u, _ = ref.step(i * 5e-3, u)
     assert np.abs(res - u).max() / np.abs(u).max() < 1e-9
+
+
+def _ring_worker(rank, world, port, Q, pairs, q_out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2209_06700_b200.runtime import stage_groups
+        from paper_2209_06700_b200.stage_parallel import RingCombiner
+
+        rng = np.random.default_rng(5)
+        n = 37
+        X = rng.standard_normal((Q, n))
+        groups = stage_groups(Q, world)
+        ring = RingCombiner(groups, rank, world)
+        lo, hi = groups[rank]
+        out = {}
+        D = rng.standard_normal((Q, Q))
+        out["square"] = ring(D, torch.from_numpy(X[lo:hi].copy())).numpy()
+        if pairs:  # stage groups -> paired rows (the complex path's S^-1 combine) and back
+            P = (Q + 1) // 2
+            pg = [(2 * a, 2 * b) for a, b in stage_groups(P, world)]
+            Wf = rng.standard_normal((2 * P, Q))
+            out["fwd"] = ring(Wf, torch.from_numpy(X[lo:hi].copy()), in_groups=groups, out_groups=pg).numpy()
+            Y = rng.standard_normal((2 * P, n))
+            plo, phi = pg[rank]
+            Wb = rng.standard_normal((Q, 2 * P))
+            out["back"] = ring(Wb, torch.from_numpy(Y[plo:phi].copy()), in_groups=pg, out_groups=groups).numpy()
+        q_out.put((rank, out))
+    except Exception as e:  # pragma: no cover
+        q_out.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Q,world", [(7, 3), (3, 4), (5, 2)])
+def test_ring_combiner_uneven_and_empty_groups(Q, world):
+    """Stage groups of different sizes (Q=7 on 3 ranks) and empty groups (Q=3 on 4 ranks: the
+    complex path at 4 GPUs) through the double-buffered ring, against D @ x."""
+    from paper_2209_06700_b200.runtime import stage_groups
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, Q, True, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    res = dict(q.get() for _ in range(world))
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    rng = np.random.default_rng(5)
+    n = 37
+    X = rng.standard_normal((Q, n))
+    D = rng.standard_normal((Q, Q))
+    P = (Q + 1) // 2
+    Wf = rng.standard_normal((2 * P, Q))
+    Y = rng.standard_normal((2 * P, n))
+    Wb = rng.standard_normal((Q, 2 * P))
+    groups = stage_groups(Q, world)
+    pg = [(2 * a, 2 * b) for a, b in stage_groups(P, world)]
+    for r in range(world):
+        lo, hi = groups[r]
+        plo, phi = pg[r]
+        np.testing.assert_allclose(res[r]["square"], (D @ X)[lo:hi], rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(res[r]["fwd"], (Wf @ X)[plo:phi], rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(res[r]["back"], (Wb @ Y)[lo:hi], rtol=1e-13, atol=1e-13)
