@@ -21,6 +21,7 @@
  *   spk_transfer            prolong / restrict (+ mask, + accumulate)     fem.py:189-211, multigrid.py:171-177
  *   spk_combine             SPEC tensor_ops dense_combine (D (x) I) u
  *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
+ *   spk_band_axis / spk_gauss_l2          load_vector / l2_error            fem.py:220-273
  *   spk_mgs_partial / spk_sqrt_dev        gmres MGS with all-reduced dots   krylov.py:74-82 (+ PAPER.md:426-443)
  *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
  *   spk_mask                GridHierarchy.constrain                       fem.py:153-158
@@ -161,6 +162,18 @@ int spk_coarse_vcycle(spk_ctx* ctx, int lc, int nblk, const double* lams, double
 int spk_mgs_partial(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
                     const double* v_cur, double* out, void* stream);
 int spk_sqrt_dev(double* x, int count, void* stream);
+/* Gauss-point quadrature (load_vector / l2_error, fem.py:220-273): a banded matrix (device col0[nout],
+ * vals[nout][bw]) applied along one axis of a (A, nin, B) array, out (+)= ; and the L2 norm
+ * sqrt(sum_g w(g) (ug(g) - u_exact(g))^2) over the ng^dim tensor Gauss grid, u_exact from the device
+ * array ue or, with ue == NULL, the separable T * prod_d s1[g_d]; *out is a device scalar */
+int spk_band_axis(long long A, int nin, int nout, long long B, const int* col0, const double* vals, int bw,
+                  const double* in, double* out, int accumulate, void* stream);
+int spk_gauss_l2(spk_ctx* ctx, int dim, int ng, const double* ug, const double* w1, const double* ue,
+                 const double* s1, double T, double* out, void* stream);
+/* FP64 pipe probe (no reference counterpart; measurement only): ctas x threads threads each run
+ * 8 independent DFMA chains of 16 * iters steps = 256 * iters flops per thread; sink: >= threads
+ * doubles of device scratch (never written in practice). Timed by the caller with CUDA events. */
+int spk_fp64_probe(int ctas, int threads, int iters, double* sink, void* stream);
 /* One MGS column (krylov.py:74-82) in one call: the j+2 fused spk_mgs sweeps of w against basis[0..j]
  * (host array of device pointers), H[0..j+1, j] written to hcol (device), then v_next = w / H[j+1, j]
  * when v_next is not NULL. Same launches and order as the per-sweep calls. */

@@ -77,8 +77,17 @@ def assemble_1d(elem, n_elems, k):
     return out
 
 
+FAST = False  # banded fast path (oracle/fastband.c); the dense form below is the reference's
+FAST_MIN = 1 << 17  # smaller arrays keep the dense numpy contraction (no OpenMP fork per call)
+FAST_MIN_AXIS = 129  # the dense contraction costs n_ax per entry: the band only pays on long axes
+
+
 def contract(mat, arr, axis):
-    """Dense matrix along one tensor axis (reference fem.py:37-41)."""
+    """Dense matrix along one tensor axis (reference fem.py:37-41). With FAST (or
+    Hierarchy(fast=True)) the same product over the matrix's nonzero band only."""
+    if FAST and mat.shape[1] >= FAST_MIN_AXIS and np.size(arr) >= FAST_MIN:
+        from .fastband import band_contract
+        return band_contract(mat, arr, axis)
     moved = np.moveaxis(arr, axis, 0)
     res = mat @ moved.reshape(moved.shape[0], -1)
     return np.moveaxis(res.reshape((mat.shape[0],) + moved.shape[1:]), 0, axis)
@@ -141,9 +150,12 @@ class Level:
 class Hierarchy:
     """Oracle GridHierarchy(dim, max_level, k)."""
 
-    def __init__(self, dim, max_level, k=1):
+    def __init__(self, dim, max_level, k=1, fast=False):
         self.dim, self.max_level, self.k = dim, max_level, k
         self.levels = [Level(l, dim, k) for l in range(max_level + 1)]
+        if fast:  # process-wide switch: every contraction of the oracle takes the banded path
+            global FAST
+            FAST = True
 
     @property
     def finest(self):
@@ -162,12 +174,28 @@ class Hierarchy:
             w = contract(mat, w, off + ax)
         return w.reshape(lead + (lvl.n_dofs,))
 
+    def _mass_stiff_fast(self, level, u):
+        """(M u, K u) by sum factorisation over banded 1D factors (fast path only): the same
+        Kronecker products as apply_mass / apply_stiffness with shared partial sweeps."""
+        from .fastband import band_contract as bc
+        lvl = self.levels[level]
+        lead = u.shape[:-1]
+        off = len(lead)
+        w = np.asarray(u, dtype=float).reshape(lead + lvl.shape)
+        Mm, Kk = lvl.mass_1d, lvl.stiffness_1d
+        m, k = bc(Mm, w, off + self.dim - 1), bc(Kk, w, off + self.dim - 1)   # last axis
+        for ax in range(self.dim - 2, -1, -1):
+            m, k = bc(Mm, m, off + ax), bc(Mm, k, off + ax, out=bc(Kk, m, off + ax))
+        return m.reshape(lead + (lvl.n_dofs,)), k.reshape(lead + (lvl.n_dofs,))
+
     def apply_mass(self, level, u):
         lvl = self.levels[level]
         return self._kron_apply(level, u, [lvl.mass_1d] * self.dim)
 
     def apply_stiffness(self, level, u):
         lvl = self.levels[level]
+        if FAST and self.levels[level].n_per_axis >= FAST_MIN_AXIS:
+            return self._mass_stiff_fast(level, u)[1]
         out = 0.0
         for d in range(self.dim):
             facs = [lvl.stiffness_1d if ax == d else lvl.mass_1d for ax in range(self.dim)]
@@ -175,8 +203,11 @@ class Hierarchy:
         return out
 
     def apply_shifted(self, level, lam, tau, u):
-        mu = self.apply_mass(level, u)
-        ku = self.apply_stiffness(level, u)
+        if FAST and self.levels[level].n_per_axis >= FAST_MIN_AXIS:
+            mu, ku = self._mass_stiff_fast(level, u)
+        else:
+            mu = self.apply_mass(level, u)
+            ku = self.apply_stiffness(level, u)
         if np.ndim(lam) == 0:
             return lam * mu + tau * ku
         return np.asarray(lam).reshape((-1,) + (1,) * (np.ndim(u) - 1)) * mu + tau * ku
@@ -190,8 +221,11 @@ class Hierarchy:
         """(D_M (x) M + D_K (x) K) u on (Q, n) stage vectors (SPEC irk:A operator form)."""
         mask = self.levels[level].interior_mask
         ui = np.where(mask, u, 0.0) if constrained else u
-        mu = self.apply_mass(level, ui)
-        ku = self.apply_stiffness(level, ui)
+        if FAST and self.levels[level].n_per_axis >= FAST_MIN_AXIS:
+            mu, ku = self._mass_stiff_fast(level, ui)
+        else:
+            mu = self.apply_mass(level, ui)
+            ku = self.apply_stiffness(level, ui)
         v = np.asarray(DM) @ mu + np.asarray(DK) @ ku
         return np.where(mask, v, u) if constrained else v
 

@@ -954,6 +954,32 @@ int spk_mgs_partial(spk_ctx* c, long long n, double* w, const double* v_prev, co
   return SPK_OK;
 }
 
+int spk_band_axis(long long A, int nin, int nout, long long B, const int* col0, const double* vals, int bw,
+                  const double* in, double* out, int accumulate, void* stream) {
+  if (A < 1 || B < 1 || nin < 1 || nout < 1 || bw < 1 || bw > nin) return fail(SPK_EDIM, "band_axis: bad shape");
+  cudaError_t e = spk_launch_band_axis(A, nin, nout, B, col0, vals, bw, in, out, accumulate, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "band_axis");
+  return SPK_OK;
+}
+
+int spk_gauss_l2(spk_ctx* c, int dim, int ng, const double* ug, const double* w1, const double* ue,
+                 const double* s1, double T, double* out, void* stream) {
+  if (!c) return fail(SPK_ECONFIG, "null context");
+  if (dim < 1 || dim > 3 || ng < 1) return fail(SPK_EDIM, "gauss_l2: bad shape");
+  if (!ue && !s1) return fail(SPK_ECONFIG, "gauss_l2: need u_exact values or a separable factor");
+  if (int rc = ensure_scratch(c, spk_gauss_l2_grid())) return rc;
+  cudaError_t e = spk_launch_gauss_l2(dim, ng, ug, w1, ue, s1, T, c->partial, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gauss_l2");
+  return SPK_OK;
+}
+
+int spk_fp64_probe(int ctas, int threads, int iters, double* sink, void* stream) {
+  if (ctas < 1 || threads < 32 || threads > 1024 || iters < 1) return fail(SPK_ECONFIG, "fp64_probe: bad sizes");
+  cudaError_t e = spk_launch_fp64_probe(ctas, threads, iters, sink, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fp64_probe");
+  return SPK_OK;
+}
+
 int spk_sqrt_dev(double* x, int count, void* stream) {
   if (count < 0 || count > 32) return fail(SPK_ECONFIG, "sqrt_dev: count must lie in [0, 32]");
   cudaError_t e = spk_launch_sqrt(x, count, (cudaStream_t)stream);

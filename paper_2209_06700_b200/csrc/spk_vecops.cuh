@@ -133,6 +133,12 @@ cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
 int spk_mgs_coop_grid();
 cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s);
 cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s);
+cudaError_t spk_launch_band_axis(long long A, int nin, int nout, long long B, const int* col0, const double* vals,
+                                 int bw, const double* in, double* out, int acc, cudaStream_t s);
+int spk_gauss_l2_grid();
+cudaError_t spk_launch_gauss_l2(int dim, int ng, const double* ug, const double* w1, const double* ue,
+                                const double* s1, double T, double* partial, double* out, cudaStream_t s);
+cudaError_t spk_launch_fp64_probe(int ctas, int threads, int iters, double* sink, cudaStream_t s);
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s);
 cudaError_t spk_launch_reduce_partials(const double* partial, int m, double* out, int sqrt_out, cudaStream_t s);
 cudaError_t spk_launch_lincomb(long long n, int k, const double* const* vs, const double* y, double* z,

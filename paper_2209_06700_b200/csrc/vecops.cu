@@ -745,6 +745,77 @@ __global__ void scale_div_kernel(long long n, const double* w, const double* h, 
     v[i] = w[i] / d;
 }
 
+// ---- Gauss-point transfers (load vector / L2 error, reference fem.py:220-273) ----
+// A banded matrix (row i: entries vals[i][0..bw) at columns col0[i] + j) applied along one tensor
+// axis of a (A, nin, B) array: out[a, i, b] (+)= sum_j vals[i][j] in[a, col0[i] + j, b]. The 1D load
+// matrix (nodes x Gauss points, <= 2(k+1) entries per row) and the interpolation matrix (Gauss points
+// x nodes, k+1 per row) applied axis by axis are the tensor-product quadratures of the reference.
+__global__ void band_axis_kernel(long long A, int nin, int nout, long long B, const int* __restrict__ col0,
+                                 const double* __restrict__ vals, int bw, const double* __restrict__ in,
+                                 double* __restrict__ out, int acc) {
+  const long long total = A * nout * B;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long b = idx % B;
+    const long long ai = idx / B;
+    const int i = (int)(ai % nout);
+    const long long a = ai / nout;
+    const double* src = in + (a * nin + col0[i]) * B + b;
+    const double* v = vals + (long long)i * bw;
+    double s = 0.0;
+    for (int j = 0; j < bw; ++j) s = fma(v[j], src[(long long)j * B], s);
+    out[idx] = acc ? out[idx] + s : s;
+  }
+}
+
+// sum over the tensor Gauss grid (ng points per axis, dim axes) of w(g) (u_h(g) - u_exact(g))^2 with
+// w = prod of the 1D weights; u_exact from a device array, or separable T * prod s1[axis index]
+__global__ void __launch_bounds__(TPB) gauss_l2_kernel(int dim, int ng, const double* __restrict__ ug,
+                                                       const double* __restrict__ w1,
+                                                       const double* __restrict__ ue,
+                                                       const double* __restrict__ s1, double T,
+                                                       double* __restrict__ partial) {
+  __shared__ double red[TPB];
+  long long total = ng;
+  for (int d = 1; d < dim; ++d) total *= ng;
+  double acc = 0.0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long r = idx;
+    double w = 1.0, sx = 1.0;
+    for (int d = 0; d < dim; ++d) {
+      const int c = (int)(r % ng);
+      r /= ng;
+      w *= w1[c];
+      if (!ue) sx *= s1[c];
+    }
+    const double ex = ue ? ue[idx] : T * sx;
+    const double df = ug[idx] - ex;
+    acc = fma(w * df, df, acc);
+  }
+  const double bs = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = bs;
+}
+
+
+// ---- FP64 pipe probe: independent DFMA chains (ILP 8), the denominator of the bench's fp64_pipe ----
+__global__ void fp64_probe_kernel(double* sink, int iters, double a, double b) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 12345.678) sink[threadIdx.x] = s;  // never true: keeps the chains alive
+}
+
+
 // ---- x <- sqrt(x) for a few device scalars (distributed GMRES: all-reduced sum of squares -> norm) ----
 __global__ void sqrt_kernel(double* x, int count) {
   if (threadIdx.x < count) x[threadIdx.x] = sqrt(x[threadIdx.x]);
@@ -842,6 +913,32 @@ int grid_for(long long n) {
 }
 
 }  // namespace
+
+cudaError_t spk_launch_band_axis(long long A, int nin, int nout, long long B, const int* col0, const double* vals,
+                                 int bw, const double* in, double* out, int acc, cudaStream_t s) {
+  band_axis_kernel<<<grid_for(A * nout * B), TPB, 0, s>>>(A, nin, nout, B, col0, vals, bw, in, out, acc);
+  return cudaGetLastError();
+}
+
+int spk_gauss_l2_grid() { return 148 * 4; }
+
+cudaError_t spk_launch_gauss_l2(int dim, int ng, const double* ug, const double* w1, const double* ue,
+                                const double* s1, double T, double* partial, double* out, cudaStream_t s) {
+  gauss_l2_kernel<<<spk_gauss_l2_grid(), TPB, 0, s>>>(dim, ng, ug, w1, ue, s1, T, partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return spk_launch_reduce_partials(partial, spk_gauss_l2_grid(), out, 1, s);
+}
+
+cudaError_t spk_launch_fp64_probe(int ctas, int threads, int iters, double* sink, cudaStream_t s) {
+  fp64_probe_kernel<<<ctas, threads, 0, s>>>(sink, iters, 1.0000001, 1e-9);
+  return cudaGetLastError();
+}
+
+cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s) {
+  sqrt_kernel<<<1, 32, 0, s>>>(x, count);
+  return cudaGetLastError();
+}
 
 cudaError_t spk_launch_cheb_init(int K, const SpkVecArgs& a, cudaStream_t s) {
   const long long total = (long long)a.nblk * a.g.n;
@@ -1025,10 +1122,6 @@ cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s) {
                                      args, 0, s);
 }
 
-cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s) {
-  sqrt_kernel<<<1, 32, 0, s>>>(x, count);
-  return cudaGetLastError();
-}
 
 cudaError_t spk_launch_scale_div(long long n, const double* w, const double* h, double* v, cudaStream_t s) {
   return spk_launch(scale_div_kernel, grid_for(n), TPB, 0, s, n, w, h, v);

@@ -354,22 +354,64 @@ class GridHierarchy:
                 I[(k + 1) * e : (k + 1) * (e + 1), k * e + a] = shape[a]
         return I
 
-    def _contract_axes(self, mat, arr):
-        out = arr
-        for ax in range(self.dim):
-            out = torch.movedim(torch.tensordot(mat, out, dims=([1], [ax])), 0, ax)
-        return out
+    def _band_dev(self, key, mat):
+        """Device (col0, vals, bw) of a banded host matrix, cached per (kind, level)."""
+        cache = self.__dict__.setdefault("_bands", {})
+        ent = cache.get(key)
+        if ent is None:
+            nz = mat != 0.0
+            first = np.where(nz.any(axis=1), nz.argmax(axis=1), 0)
+            last = np.where(nz.any(axis=1), mat.shape[1] - 1 - nz[:, ::-1].argmax(axis=1), 0)
+            bw = int(max(1, (last - first + 1).max()))
+            col0 = np.minimum(first, mat.shape[1] - bw).astype(np.int32)
+            vals = np.take_along_axis(mat, col0[:, None] + np.arange(bw)[None, :], axis=1)
+            ent = (torch.from_numpy(col0).to(self.device), torch.from_numpy(np.ascontiguousarray(vals)).to(self.device),
+                   bw, mat.shape[1], mat.shape[0])
+            cache[key] = ent
+        return ent
 
-    def load_vector(self, level, f, t):
-        """Consistent load vector int f(x,t) phi_i with the (k+1)-point Gauss rule per axis
-        (reference fem.py:220-246); f is evaluated at the tensor Gauss points."""
+    def _axes_apply(self, key, mat, arr):
+        """mat applied along every axis of the (nin,)*dim device array (spk_band_axis per axis)."""
+        col0, vals, bw, nin, nout = self._band_dev(key, mat)
+        st = stream_ptr(self.device)
+        cur = arr.contiguous()
+        for ax in range(self.dim):
+            shp = list(cur.shape)
+            A = int(np.prod(shp[:ax], dtype=np.int64))
+            B = int(np.prod(shp[ax + 1 :], dtype=np.int64))
+            shp[ax] = nout
+            out = torch.empty(shp, dtype=torch.float64, device=self.device)
+            _lib.call("spk_band_axis", A, nin, nout, B, ptr(col0), ptr(vals), bw, ptr(cur), ptr(out), 0, st)
+            cur = out
+        return cur
+
+    def _gauss_points(self, level):
         pts1, _, _, _ = self._gauss_axis(level)
         mesh = np.meshgrid(*([pts1] * self.dim), indexing="ij")
-        pts = np.stack([m.ravel() for m in mesh], axis=-1)
-        fv = torch.from_numpy(np.asarray(f(pts, t), dtype=float).reshape((pts1.size,) * self.dim))
-        B = torch.from_numpy(self.load_matrix_1d(level)).to(self.device)
-        out = self._contract_axes(B, fv.to(self.device))
-        return out.reshape(-1).cpu().numpy()
+        return pts1, np.stack([m.ravel() for m in mesh], axis=-1)
+
+    def load_vector_device(self, level, f, t):
+        """Device (n,) consistent load vector int f(x,t) phi_i, (k+1)-point Gauss rule per axis
+        (reference fem.py:220-246). Separable sources (SeparableSolution, and the reference's
+        `manufactured()` family, which carry `.separable`) are formed on the device from the 1D
+        load vector (spk_outer3, times F(t)); general callables are evaluated on the host at the
+        tensor Gauss points (they are user numpy code) and contracted by the device Gauss-to-node
+        kernel (spk_band_axis along each axis)."""
+        sep = getattr(f, "separable", None)
+        if sep is not None:
+            g1 = torch.from_numpy(self.load_vector_1d(level, sep.s)).to(self.device)
+            out = torch.empty(self.levels[level].n_dofs, dtype=torch.float64, device=self.device)
+            _lib.call("spk_outer3", self._ctx, level, ptr(g1), ptr(out), stream_ptr(self.device))
+            return out.mul_(float(sep.F(t)))
+        pts1, pts = self._gauss_points(level)
+        fv = torch.from_numpy(np.ascontiguousarray(np.asarray(f(pts, t), dtype=float))).to(self.device)
+        out = self._axes_apply(("load", level), self.load_matrix_1d(level), fv.reshape((pts1.size,) * self.dim))
+        return out.reshape(-1)
+
+    def load_vector(self, level, f, t):
+        """Host (numpy) load vector, as the reference returns it (fem.py:220-246); the arithmetic
+        runs on the device (load_vector_device)."""
+        return self.load_vector_device(level, f, t).cpu().numpy()
 
     def load_vector_1d(self, level, s):
         """1D load vector of a spatial factor s(x) (separable sources: F = prod_a g[i_a])."""
@@ -377,21 +419,28 @@ class GridHierarchy:
         return self.load_matrix_1d(level) @ np.asarray(s(pts1), dtype=float)
 
     def l2_error(self, level, u_nodal, u_exact, t):
-        """L2 norm of u_h - u_exact by per-cell (k+1)^dim Gauss quadrature (reference fem.py:248-273)."""
+        """L2 norm of u_h - u_exact by per-cell (k+1)^dim Gauss quadrature (reference fem.py:248-273):
+        u_h interpolated to the tensor Gauss points on the device (spk_band_axis), then one fused
+        weighted-square reduction (spk_gauss_l2) with u_exact evaluated in the kernel for separable
+        solutions or taken from host evaluation at the Gauss points otherwise."""
         lvl = self.levels[level]
         pts1, _, wg, _ = self._gauss_axis(level)
-        I = torch.from_numpy(self.interp_matrix_1d(level)).to(self.device)
         u = to_device(u_nodal, self.device).reshape(lvl.shape)
-        ug = self._contract_axes(I, u)
-        mesh = np.meshgrid(*([pts1] * self.dim), indexing="ij")
-        pts = np.stack([m.ravel() for m in mesh], axis=-1)
-        ue = torch.from_numpy(np.asarray(u_exact(pts, t), dtype=float)).to(self.device)
-        diff = ug.reshape(-1) - ue
+        ug = self._axes_apply(("interp", level), self.interp_matrix_1d(level), u)
         w1 = torch.from_numpy(np.tile(wg * lvl.h, lvl.n_elements)).to(self.device)
-        wt = w1
-        for _ in range(self.dim - 1):
-            wt = torch.outer(wt, w1).reshape(-1)
-        return float(torch.sqrt(torch.sum(wt * diff * diff)).item())
+        out = torch.empty(1, dtype=torch.float64, device=self.device)
+        sep = getattr(u_exact, "separable", None)
+        st = stream_ptr(self.device)
+        if sep is not None:
+            s1 = torch.from_numpy(np.asarray(sep.s(pts1), dtype=float)).to(self.device)
+            _lib.call("spk_gauss_l2", self._ctx, self.dim, pts1.size, ptr(ug), ptr(w1), None, ptr(s1),
+                      float(sep.T(t)), ptr(out), st)
+        else:
+            _, pts = self._gauss_points(level)
+            ue = torch.from_numpy(np.ascontiguousarray(np.asarray(u_exact(pts, t), dtype=float))).to(self.device)
+            _lib.call("spk_gauss_l2", self._ctx, self.dim, pts1.size, ptr(ug), ptr(w1), ptr(ue), None, 0.0,
+                      ptr(out), st)
+        return float(out.item())
 
 
 def build_hierarchy(dim, max_level, degree=1, device=None):
@@ -422,6 +471,12 @@ def manufactured(dim):
     def f_source(x, t):
         return spatial(x) * (dT(t) + 4.0 * np.pi ** 2 * dim * T(t))
 
+    # the same functions in separable form (u = T(t) prod s(x_d), f = F(t) prod s(x_d)): device
+    # load vectors, right-hand sides and L2 errors use it (load_vector_device, irk.StageSystem)
+    sep = SeparableSolution(dim, s=lambda x: np.sin(2.0 * np.pi * np.asarray(x)), T=T,
+                            F=lambda t: dT(t) + 4.0 * np.pi ** 2 * dim * T(t))
+    u_exact.separable, f_source.separable = sep.field_view(sep.T), sep.field_view(sep.F)
+    u_exact.solution = f_source.solution = sep
     return u_exact, f_source, u_exact
 
 
@@ -442,6 +497,11 @@ class SeparableSolution:
             self.T = lambda t: np.exp(-t)
             self.F = lambda t: (d * np.pi ** 2 - 1.0) * np.exp(-t)
 
+    def field_view(self, time_factor):
+        """One separable field time_factor(t) prod s(x_d) (u: T, the source f: F) in the form the
+        device quadratures read (.s and the time factor as both .T and .F)."""
+        return SeparableSolution(self.dim, s=self.s, T=time_factor, F=time_factor)
+
     def callables(self):
         def spatial(x):
             x = np.atleast_2d(x)
@@ -450,8 +510,11 @@ class SeparableSolution:
                 v = v * self.s(x[:, d])
             return v
 
-        return (lambda x, t: spatial(x) * self.T(t), lambda x, t: spatial(x) * self.F(t),
-                lambda x, t: spatial(x) * self.T(t))
+        u = lambda x, t: spatial(x) * self.T(t)
+        f = lambda x, t: spatial(x) * self.F(t)
+        u.separable, f.separable = self.field_view(self.T), self.field_view(self.F)
+        u.solution = f.solution = self
+        return (u, f, u)
 
 
 @dataclass

@@ -64,6 +64,10 @@ class StageSystem:
         sp = spectral_real(L)
         self.lams, self.S, self.Sinv = sp.lambdas, sp.S, sp.Sinv
         self.source = source if source is not None else SeparableSolution(hierarchy.dim)
+        if isinstance(self.source, tuple) and getattr(self.source[1], "solution", None) is not None:
+            # callables of a separable solution (the reference's manufactured(), HeatProblem
+            # defaults): the device right-hand side kernel (spk_rhs) serves them
+            self.source = self.source[1].solution
         self.level = hierarchy.max_level
         lvl = hierarchy.levels[self.level]
         self.n = lvl.n_dofs
@@ -94,8 +98,7 @@ class StageSystem:
                       ptr(out), stream_ptr(h.device))
         else:
             f = self.source[1] if isinstance(self.source, tuple) else self.source.f_source
-            w = torch.stack([torch.from_numpy(h.load_vector(L, f, t_n + cj * self.tau)).to(h.device) - ku[0]
-                             for cj in self.c])
+            w = torch.stack([h.load_vector_device(L, f, t_n + cj * self.tau) - ku[0] for cj in self.c])
             dense_combine(self.Ainv, w, out=out, mask_level=L, hierarchy=h)
         return out
 

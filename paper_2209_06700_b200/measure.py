@@ -83,6 +83,23 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def fp64_peak_tflops(reps=3):
+    """DFMA throughput of this GPU, measured now (spk_fp64_probe: 8 independent chains per thread,
+    2 x 512-thread CTAs per SM): the denominator of the bench line's fp64_pipe fraction."""
+    from . import _lib
+    from ._device import stream_ptr
+
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    ctas, threads, iters = 2 * sms, 512, 4096
+    sink = torch.empty(1024, dtype=torch.float64, device="cuda")
+    st = stream_ptr(sink.device)
+    run = lambda: _lib.call("spk_fp64_probe", ctas, threads, iters, sink.data_ptr(), st)
+    run()
+    best = min(event_time(run) for _ in range(reps))
+    flops = 2.0 * 8 * 16 * iters * ctas * threads
+    return flops / (best * 1e-3) / 1e12
+
+
 def event_time(fn, stream=None):
     """Run fn() between two CUDA events on the current stream; returns milliseconds."""
     s = stream or torch.cuda.current_stream()

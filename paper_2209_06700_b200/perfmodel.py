@@ -112,3 +112,70 @@ def write_solve_log(path, rows):
         for r in rows:
             w.writerow(r)
     return path
+
+
+# ---- algorithmic HBM bytes of one Radau IIA step (SURVEY.md §8(d) "per-step model") ----------------
+# Each math operation is counted at its minimal traffic (every operand vector read once, every result
+# written once, 8 B per fp64 entry), whatever kernel split the device path uses; per-level Chebyshev /
+# V-cycle counts follow multigrid.py:74-129. Levels at or below `fused_level` run inside one CTA
+# (shared memory) and contribute nothing beyond their right-hand side and solution.
+
+def vcycle_bytes(level_dofs, deg, fused_level=-1):
+    """Bytes per block of one V-cycle over levels level_dofs[0..L] (DoFs per level, coarsest first)."""
+    tot = 0.0
+    for lvl in range(len(level_dofs) - 1, 0, -1):
+        n = float(level_dofs[lvl])
+        if lvl <= fused_level:
+            tot += 16.0 * n          # the fused cycle reads b_lc, writes x_lc
+            break
+        pre = 16.0 + 48.0 * (deg - 1)        # d = Dinv b / theta; deg-1 steps (x, r, d read + written)
+        post = 32.0 + 48.0 * (deg - 1)       # r = b - A x, d = Dinv r / theta; deg-1 steps
+        resid = 24.0 + 8.0 + 8.0 / 8.0       # r = b - A x; restrict (read r, write the coarse rhs)
+        prolong = 16.0 + 8.0 / 8.0           # x += P e_c
+        tot += n * (pre + post + resid + prolong)
+    else:
+        tot += 16.0 * float(level_dofs[0])   # direct coarse solve (dense inverse: small)
+    return tot
+
+
+def gmres_bytes(N, its):
+    """MGS columns (krylov.py:74-82), basis scaling, the final sum_i y_i v_i, the true residual."""
+    tot = 16.0 * N                                     # beta = ||b||
+    for j in range(its):
+        tot += N * (16.0 + 32.0 * j + 24.0 + 16.0)     # <v0,w>; j fused (axpy, dot); last axpy + norm; scale
+    tot += 8.0 * (its + 1) * N                         # sum_i y_i v_i
+    tot += 24.0 * N                                    # ||b - A x||
+    return tot
+
+
+def real_step_bytes(level_dofs, Q, deg, its, fused_level=-1):
+    """Real LU path (irk.StageSystem): rhs, (its + 1) x [A P^-1], GMRES, update."""
+    n = float(level_dofs[-1])
+    N = Q * n
+    rhs = 16.0 * n + 8.0 * n + 8.0 * N                 # K u_n; source / A^-1 mix of Q rows
+    pinv = 16.0 * N + Q * vcycle_bytes(level_dofs, deg, fused_level) + 16.0 * N   # S~^-1, V-cycles, S~
+    op = 16.0 * N                                      # K1 coupled (A^-1 (x) M + tau I (x) K)
+    update = 8.0 * (Q + 2) * n
+    return rhs + (its + 1) * (pinv + op) + gmres_bytes(N, its) + update
+
+
+def complex_step_bytes(level_dofs, Q, deg, block_its, variant="presb", fused_level=-1):
+    """Direct complex path (complex_solver.DirectComplexSystem): rhs, S^-1, per pair block GMRES on
+    the real 2x2 form with PRESB (2 V-cycles + 1 apply + 4 vector passes) or the 2x2 V-cycle, the real
+    block with the plain V-cycle, S, update. block_its: GMRES iterations per block (pairs first)."""
+    n = float(level_dofs[-1])
+    N = Q * n
+    tot = 16.0 * n + 8.0 * n + 8.0 * N + 2.0 * 16.0 * N + 8.0 * (Q + 2) * n
+    npairs = Q // 2
+    vc = vcycle_bytes(level_dofs, deg, fused_level)
+    for b, its in enumerate(block_its):
+        pair = b < npairs
+        rows = 2 if pair else 1
+        if pair and variant == "presb":
+            pc = 2.0 * vc + 16.0 * n + 4.0 * 24.0 * n
+        elif pair:
+            pc = 2.0 * vc
+        else:
+            pc = vc
+        tot += (its + 1) * (pc + 16.0 * rows * n) + gmres_bytes(rows * n, its)
+    return tot
