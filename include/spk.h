@@ -21,6 +21,7 @@
  *   spk_transfer            prolong / restrict (+ mask, + accumulate)     fem.py:189-211, multigrid.py:171-177
  *   spk_combine             SPEC tensor_ops dense_combine (D (x) I) u
  *   spk_mgs / spk_scale_div / spk_lincomb  gmres MGS, basis, final update  krylov.py:69-93
+ *   spk_givens                            gmres least-squares residual       krylov.py:84-87, :106-110
  *   spk_band_axis / spk_gauss_l2          load_vector / l2_error            fem.py:220-273
  *   spk_mgs_partial / spk_sqrt_dev        gmres MGS with all-reduced dots   krylov.py:74-82 (+ PAPER.md:426-443)
  *   spk_rhs / spk_outer3 / spk_update      SPEC irk_solver.assemble_rhs / step
@@ -162,6 +163,10 @@ int spk_coarse_vcycle(spk_ctx* ctx, int lc, int nblk, const double* lams, double
 int spk_mgs_partial(spk_ctx* ctx, long long n, double* w, const double* v_prev, const double* h_prev,
                     const double* v_cur, double* out, void* stream);
 int spk_sqrt_dev(double* x, int count, void* stream);
+/* GMRES least-squares residual on the device (krylov.py:84-87): column j of H (hcol, j+2 entries,
+ * not modified) rotated by the previous Givens rotations (cs: 2 per column) into rcol, a new rotation
+ * for H[j+1, j], g (the rotated beta e_1) updated, *res = |g[j+1]| = the lstsq residual norm */
+int spk_givens(const double* hcol, double* rcol, double* cs, double* g, double* res, int j, void* stream);
 /* Gauss-point quadrature (load_vector / l2_error, fem.py:220-273): a banded matrix (device col0[nout],
  * vals[nout][bw]) applied along one axis of a (A, nin, B) array, out (+)= ; and the L2 norm
  * sqrt(sum_g w(g) (ug(g) - u_exact(g))^2) over the ng^dim tensor Gauss grid, u_exact from the device

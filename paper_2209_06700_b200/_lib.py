@@ -73,6 +73,7 @@ _SIGS = {
     "spk_mgs_partial": ([c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "spk_sqrt_dev": ([c_vp, c_int, c_vp], c_int),
     "spk_fp64_probe": ([c_int, c_int, c_int, c_vp, c_vp], c_int),
+    "spk_givens": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp], c_int),
     "spk_band_axis": ([c_ll, c_int, c_int, c_ll, c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp], c_int),
     "spk_gauss_l2": ([c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_vp], c_int),
     "spk_scale_div": ([c_ll, c_vp, c_vp, c_vp, c_vp], c_int),

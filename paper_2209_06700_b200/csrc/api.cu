@@ -973,6 +973,13 @@ int spk_gauss_l2(spk_ctx* c, int dim, int ng, const double* ug, const double* w1
   return SPK_OK;
 }
 
+int spk_givens(const double* hcol, double* rcol, double* cs, double* g, double* res, int j, void* stream) {
+  if (j < 0) return fail(SPK_ECONFIG, "givens: bad column");
+  cudaError_t e = spk_launch_givens(hcol, rcol, cs, g, res, j, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "givens");
+  return SPK_OK;
+}
+
 int spk_fp64_probe(int ctas, int threads, int iters, double* sink, void* stream) {
   if (ctas < 1 || threads < 32 || threads > 1024 || iters < 1) return fail(SPK_ECONFIG, "fp64_probe: bad sizes");
   cudaError_t e = spk_launch_fp64_probe(ctas, threads, iters, sink, (cudaStream_t)stream);

@@ -133,6 +133,8 @@ cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s);
 int spk_mgs_coop_grid();
 cudaError_t spk_launch_mgs_column_coop(const SpkMgsColArgs& a, cudaStream_t s);
 cudaError_t spk_launch_sqrt(double* x, int count, cudaStream_t s);
+cudaError_t spk_launch_givens(const double* hcol, double* rcol, double* cs, double* g, double* res, int j,
+                              cudaStream_t s);
 cudaError_t spk_launch_band_axis(long long A, int nin, int nout, long long B, const int* col0, const double* vals,
                                  int bw, const double* in, double* out, int acc, cudaStream_t s);
 int spk_gauss_l2_grid();

@@ -268,7 +268,7 @@ __device__ __forceinline__ void elem3(const Coef<K>& cf, const double (&La)[K + 
 
 // Fused epilogue at one node for all Q stages / blocks of the CTA. Block mode: stage q of the CTA is
 // block b0 + q with its own shift lam[q] (and Chebyshev coefficients in its parameter slot).
-template <int K, int Q, bool BLOCK, int EPI>
+template <int K, int Q, bool BLOCK, int EPI, bool FULL = false>
 __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const double (&lamq)[Q],
                                          const double* dtab, const double (&ith)[Q], int x, int y, int z,
                                          long long gi, const double (&val)[Q], double& sumsq,
@@ -282,8 +282,8 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
   const long long vbase = (BLOCK ? (long long)b0 * a.sv : 0) + gi;
   const int slot0 = BLOCK ? b0 - a.blk_base : 0;
   const bool vsplit = BLOCK && a.vplanes != 0;
-  const bool bnd_yz = a.constrained && ((g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
-                                        (g.Ez > 0 && (z == 0 || z == g.nz - 1)));
+  const bool bnd_yz = !FULL && a.constrained && ((g.Ey > 0 && (y == 0 || y == g.ny - 1)) ||
+                                                 (g.Ez > 0 && (z == 0 || z == g.nz - 1)));
   bool bndq[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -399,32 +399,34 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
   }
 }
 
-template <int K, int Q, bool BLOCK, int EPI>
-__global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB : ((EPI == EPI_STORE || Q <= 2) ? Geo<K, Q>::MINB : 1))
-    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
+// FULL: the CTA's (y, z) tile and its loaded halo lie strictly inside the domain (no zero-filled
+// slots, no missing neighbour elements, no constrained y/z boundary rows): every per-item bound
+// check and boundary weight is compile-time (measured: the predicate / select overhead of the
+// generic body is a visible share of K1's issue slots).
+template <int K, int Q, bool BLOCK, int EPI, bool FULL>
+__device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* smem) {
   using G = Geo<K, Q>;
   constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;
   constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
   constexpr int PPT = G::PPT;
 
-  extern __shared__ double smem[];
   double* Us = smem;                    // [2][Q][NYin][NZp]
-  double* ABs = Us + 2 * G::U_SZ;       // [2][A|B][Q][NYin][TZp]
-  double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][MA|C][Q][TY][TZp]
+  double* ABs = Us + 2 * G::U_SZ;       // [2][Q][NYin][TZp] of (A, B) pairs (16-byte accesses)
+  double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][Q][TY][TZp] of (MA, C) pairs
   double* dtab = MCs + 2 * G::NBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
 
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
-  const bool ydeg = (g.Ey == 0), xdeg = (g.Ex == 0);
+  const bool ydeg = !FULL && (g.Ey == 0), xdeg = !FULL && (g.Ex == 0);
   const int ez0 = blockIdx.x * TZE, ey0 = blockIdx.y * TYE;
   const int chunk = blockIdx.z % a.nchunks;
   const int b0 = BLOCK ? (a.blk_base + (int)(blockIdx.z / a.nchunks) * Q) : 0;  // first block of CTA
 
   const int z_lo = K * ez0, z_hi = min(K * (ez0 + TZE), g.nz);
   const int y_lo = ydeg ? 0 : K * ey0, y_hi = ydeg ? 1 : min(K * (ey0 + TYE), g.ny);
-  const int nzo = z_hi - z_lo, nyo = y_hi - y_lo;
-  const int nez = min(TZE, g.Ez + 1 - ez0);            // includes the virtual last-vertex element
-  const int ney = ydeg ? 1 : min(TYE, g.Ey + 1 - ey0);
+  const int nzo = FULL ? TZ : z_hi - z_lo, nyo = FULL ? TY : y_hi - y_lo;
+  const int nez = FULL ? TZE : min(TZE, g.Ez + 1 - ez0);  // includes the virtual last-vertex element
+  const int ney = FULL ? TYE : (ydeg ? 1 : min(TYE, g.Ey + 1 - ey0));
   const double* __restrict__ u = a.u + (BLOCK ? (long long)b0 * a.su : 0);
 
   double lamq[Q];
@@ -497,8 +499,8 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
     const bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
     const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
-    loff[i] = in ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
-    if (!in || (a.constrained && bnd)) lzero |= 1u << i;
+    loff[i] = (FULL || in) ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
+    if (!FULL && (!in || (a.constrained && bnd))) lzero |= 1u << i;
 #pragma unroll
     for (int qq = 0; qq < Q; ++qq)
       if (q == qq) lq[qq] |= 1u << i;
@@ -586,14 +588,12 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   auto zphase = [&](auto PB) {
     const int ub = parity_of(PB), ab = ub;
     const double* Ub = Us + ub * G::U_SZ;
-    double* As = ABs + ab * 2 * G::AB_SZ;
-    double* Bs = As + G::AB_SZ;
+    double2* AB = reinterpret_cast<double2*>(ABs + ab * 2 * G::AB_SZ);
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
       if (zeb[i] >= nez) continue;
       const double* row = Ub + zoff[i] * NZp;
-      double* arow = As + zoff[i] * TZp;
-      double* brow = Bs + zoff[i] * TZp;
+      double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
       double L[K + 1], R[K + 1];
 #pragma unroll
@@ -606,14 +606,13 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 #pragma unroll
           for (int s = 1; s <= K; ++s) R[s] = row[K * e + K + s];
           const int ez = ez0 + e;
-          const double wl = ez > 0 ? 1.0 : 0.0, wr = ez < g.Ez ? 1.0 : 0.0;
+          const double wl = (FULL || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
           double oa[K], ob[K];
           elem2<K>(cf, L, R, wl, wr, oa, ob);
 #pragma unroll
           for (int r = 0; r < K; ++r) {
             const int zl = K * e + r;
-            arow[zl] = oa[r];  // zl < TZ always; columns >= nzo are never read
-            brow[zl] = ob[r];
+            abrow[zl] = make_double2(oa[r], ob[r]);  // zl < TZ always; columns >= nzo are never read
           }
 #pragma unroll
           for (int s = 0; s <= K; ++s) L[s] = R[s];
@@ -625,17 +624,12 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   // ---------------- Y-phase: MA = My A, C = Ky A + My B ----------------
   auto yphase = [&](auto PB) {
     const int ab = parity_of(PB), mc = ab;
-    const double* As = ABs + ab * 2 * G::AB_SZ;
-    const double* Bs = As + G::AB_SZ;
-    double* MAs = MCs + mc * 2 * G::MC_SZ;
-    double* Cs = MAs + G::MC_SZ;
+    const double2* AB = reinterpret_cast<const double2*>(ABs + ab * 2 * G::AB_SZ);
+    double2* MC = reinterpret_cast<double2*>(MCs + mc * 2 * G::MC_SZ);
     if (ydeg) {
       for (int it = tid; it < Q * TZ; it += NT) {
         const int q = it / TZ, zl = it - q * TZ;
-        if (zl < nzo) {
-          MAs[(q * TY) * TZp + zl] = As[(q * NYin + K) * TZp + zl];
-          Cs[(q * TY) * TZp + zl] = Bs[(q * NYin + K) * TZp + zl];
-        }
+        if (zl < nzo) MC[(q * TY) * TZp + zl] = AB[(q * NYin + K) * TZp + zl];
       }
       return;
     }
@@ -643,16 +637,15 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     for (int i = 0; i < G::YIT; ++i) {
       if (yeb[i] >= ney) continue;
       const int q = yoff[i] >> 12, zl = yoff[i] & 4095;
-      const double* acol = As + (q * NYin) * TZp + zl;
-      const double* bcol = Bs + (q * NYin) * TZp + zl;
-      double* mcol = MAs + (q * TY) * TZp + zl;
-      double* ccol = Cs + (q * TY) * TZp + zl;
+      const double2* abcol = AB + (q * NYin) * TZp + zl;
+      double2* mccol = MC + (q * TY) * TZp + zl;
       const int e_beg = yeb[i];
       double La[K + 1], Ra[K + 1], Lb[K + 1], Rb[K + 1];
 #pragma unroll
       for (int s = 0; s <= K; ++s) {
-        La[s] = acol[(K * e_beg + s) * TZp];
-        Lb[s] = bcol[(K * e_beg + s) * TZp];
+        const double2 t = abcol[(K * e_beg + s) * TZp];
+        La[s] = t.x;
+        Lb[s] = t.y;
       }
 #pragma unroll
       for (int el = 0; el < G::YS; ++el) {
@@ -662,18 +655,18 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
           Rb[0] = Lb[K];
 #pragma unroll
           for (int s = 1; s <= K; ++s) {
-            Ra[s] = acol[(K * e + K + s) * TZp];
-            Rb[s] = bcol[(K * e + K + s) * TZp];
+            const double2 t = abcol[(K * e + K + s) * TZp];
+            Ra[s] = t.x;
+            Rb[s] = t.y;
           }
           const int ey = ey0 + e;
-          const double wl = ey > 0 ? 1.0 : 0.0, wr = ey < g.Ey ? 1.0 : 0.0;
+          const double wl = (FULL || ey > 0) ? 1.0 : 0.0, wr = (FULL || ey < g.Ey) ? 1.0 : 0.0;
           double om[K], oc[K];
           elem3<K>(cf, La, Ra, Lb, Rb, wl, wr, om, oc);
 #pragma unroll
           for (int r = 0; r < K; ++r) {
             const int yl = K * e + r;  // yl < TY always; rows >= nyo are never read
-            mcol[yl * TZp] = om[r];
-            ccol[yl * TZp] = oc[r];
+            mccol[yl * TZp] = make_double2(om[r], oc[r]);
           }
 #pragma unroll
           for (int s = 0; s <= K; ++s) { La[s] = Ra[s]; Lb[s] = Rb[s]; }
@@ -692,7 +685,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     pyl[j] = p / TZ;
     pzl[j] = p - pyl[j] * TZ;
     pyz[j] = (y_lo + pyl[j]) * g.nz + (z_lo + pzl[j]);
-    pv[j] = (p < TY * TZ) && pyl[j] < nyo && pzl[j] < nzo;
+    pv[j] = (p < TY * TZ) && (FULL || (pyl[j] < nyo && pzl[j] < nzo));
 #pragma unroll
     for (int q = 0; q < Q; ++q)
 #pragma unroll
@@ -704,11 +697,10 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
   // ---------------- X-phase: stage mix + element-push accumulation ----------------
   // the plane's local index r within element ecur is uniform: dispatch to a copy with the x-table
   // column as compile-time register operands
-  auto xphase_r = [&](auto RC, int x, auto MC) {
-    const int mc = parity_of(MC);
+  auto xphase_r = [&](auto RC, int x, auto MCP) {
+    const int mc = parity_of(MCP);
     constexpr int RR = decltype(RC)::value;
-    const double* MAs = MCs + mc * 2 * G::MC_SZ;
-    const double* Cs = MAs + G::MC_SZ;
+    const double2* MC = reinterpret_cast<const double2*>(MCs + mc * 2 * G::MC_SZ);
     constexpr int r_loc = RR;
     double cmx[K + 1], ckx[K + 1];
 #pragma unroll
@@ -723,8 +715,9 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
       double ma[Q], cc[Q], pq[Q], qq[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        ma[q] = MAs[(q * TY + yl) * TZp + zl];
-        cc[q] = Cs[(q * TY + yl) * TZp + zl];
+        const double2 t = MC[(q * TY + yl) * TZp + zl];
+        ma[q] = t.x;
+        cc[q] = t.y;
       }
       if constexpr (BLOCK) {
 #pragma unroll
@@ -762,7 +755,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
       }
       const int y = y_lo + yl, z = z_lo + zl;
       if (xdeg) {
-        epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, 0, y, z, (long long)pyz[j], pq, sumsq);
+        epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, 0, y, z, (long long)pyz[j], pq, sumsq);
         continue;
       }
 #pragma unroll
@@ -778,7 +771,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 #pragma unroll
             for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
             const int xx = K * ecur + s;
-            epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, xx, y, z,
+            epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, xx, y, z,
                                        (long long)xx * plane_stride + pyz[j], val, sumsq);
           }
         }
@@ -787,7 +780,7 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
           // virtual x-split: only the last range owns it (the others' is the next range's plane 0)
-          epilogue<K, Q, BLOCK, EPI>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
+          epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
                                      (long long)(K * g.Ex) * plane_stride + pyz[j], val, sumsq,
                                      (BLOCK && a.vplanes) ? Q - 1 : 0);
         }
@@ -867,6 +860,31 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
       a.partial[cta] = red[0];
     }
   }
+}
+
+#ifndef SPK_FULL_TILES
+#define SPK_FULL_TILES 1
+#endif
+
+template <int K, int Q, bool BLOCK, int EPI>
+__global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB : ((EPI == EPI_STORE || Q <= 2) ? Geo<K, Q>::MINB : 1))
+    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  using G = Geo<K, Q>;
+  if constexpr (SPK_FULL_TILES) {
+    // the loaded rows are y in [K (ey0 - 1), K (ey0 + TYE)] (same for z): inside the domain, every
+    // element of the tile real (ey0 >= 1, ey0 + TYE <= Ey), and away from the constrained boundary
+    const SpkDims& g = a.g;
+    const int ez0 = blockIdx.x * G::TZE, ey0 = blockIdx.y * G::TYE;
+    const int lo = a.constrained ? 2 : 1, hi = a.constrained ? 1 : 0;
+    const bool full = g.Ey > 0 && g.Ez > 0 && g.Ex > 0 && ey0 >= lo && ez0 >= lo && ey0 + G::TYE + hi <= g.Ey &&
+                      ez0 + G::TZE + hi <= g.Ez;
+    if (full) {
+      stage_apply_body<K, Q, BLOCK, EPI, true>(a, smem);
+      return;
+    }
+  }
+  stage_apply_body<K, Q, BLOCK, EPI, false>(a, smem);
 }
 
 

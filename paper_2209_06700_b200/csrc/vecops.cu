@@ -798,6 +798,35 @@ __global__ void __launch_bounds__(TPB) gauss_l2_kernel(int dim, int ng, const do
 }
 
 
+// ---- GMRES least-squares state on the device (krylov.py:84-87 stopping test without the host) ----
+// Column j of the Hessenberg matrix (hcol, j+2 entries, left untouched for the final host lstsq) is
+// rotated by the j previous Givens rotations into rcol, a new rotation annihilates H[j+1, j], and the
+// rotated right-hand side g gives the least-squares residual |g[j+1]| (= the reference's
+// ||g - H y|| from lstsq, in exact arithmetic), written to res[0]. One thread: j <= max_iter.
+__global__ void givens_kernel(const double* __restrict__ hcol, double* __restrict__ rcol, double* cs, double* g,
+                              double* res, int j) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double hi = hcol[0];
+  for (int i = 0; i < j; ++i) {
+    const double c = cs[2 * i], s = cs[2 * i + 1];
+    const double hn = hcol[i + 1];
+    const double hi1 = -s * hi + c * hn;
+    rcol[i] = c * hi + s * hn;
+    hi = hi1;
+  }
+  const double hl = hcol[j + 1];
+  const double r = hypot(hi, hl);
+  const double c = r > 0.0 ? hi / r : 1.0, s = r > 0.0 ? hl / r : 0.0;
+  cs[2 * j] = c;
+  cs[2 * j + 1] = s;
+  rcol[j] = r;
+  rcol[j + 1] = 0.0;
+  const double gj = g[j];
+  g[j] = c * gj;
+  g[j + 1] = -s * gj;
+  res[0] = fabs(g[j + 1]);
+}
+
 // ---- FP64 pipe probe: independent DFMA chains (ILP 8), the denominator of the bench's fp64_pipe ----
 __global__ void fp64_probe_kernel(double* sink, int iters, double a, double b) {
   double acc[8];
@@ -928,6 +957,12 @@ cudaError_t spk_launch_gauss_l2(int dim, int ng, const double* ug, const double*
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return spk_launch_reduce_partials(partial, spk_gauss_l2_grid(), out, 1, s);
+}
+
+cudaError_t spk_launch_givens(const double* hcol, double* rcol, double* cs, double* g, double* res, int j,
+                              cudaStream_t s) {
+  givens_kernel<<<1, 32, 0, s>>>(hcol, rcol, cs, g, res, j);
+  return cudaGetLastError();
 }
 
 cudaError_t spk_launch_fp64_probe(int ctas, int threads, int iters, double* sink, cudaStream_t s) {

@@ -20,7 +20,7 @@ from . import _lib
 from ._device import ptr, stream_ptr
 from .errors import ConfigurationError, StepFailureError
 from .fem import SeparableSolution
-from .krylov import gmres
+from .krylov import GraphedIterations, gmres
 from .multigrid import BatchedBlockSolver, MultiBlockSolver, VCycleConfig
 from .tableau import crout_lu, radau_iia, spectral_real
 from .tensor_ops import dense_combine
@@ -84,6 +84,10 @@ class StageSystem:
         # host-bound small problems: overlap the host least squares with the next A P^{-1} product
         # (krylov.gmres(speculate=True); costs one discarded application per solve)
         self.speculate = self.Q * self.n <= SPECULATE_MAX_DOFS
+        # ... and run their GMRES iterations as replayed per-iteration CUDA graphs with the residual
+        # test on the device (krylov.GraphedIterations); large problems are device-bound already
+        self.graph_iterations = self.speculate and self._real_path
+        self._gi = None
 
     # ---- pieces ----
     def assemble_rhs(self, t_n, u_n):
@@ -129,13 +133,25 @@ class StageSystem:
         self._graph.replay()
         return self._g_out
 
+    def _graphed_iterations(self):
+        if not (self.graph_iterations and self.use_graphs):
+            return None
+        if self._gi is None:
+            self._gi = GraphedIterations(self.apply_system_operator, lambda r: self._precond_body(r, None),
+                                         (self.Q, self.n), self.h.device, self.max_iter)
+        return self._gi
+
     def step(self, t_n, u_n, check=True):
         """u_{n+1} for device u_n (n,), and the SolveReport."""
         rhs = self.assemble_rhs(t_n, u_n)
         v0 = self.vcycles
+        gi = self._graphed_iterations()
         k, rep = gmres(self.apply_system_operator, self.apply_preconditioner, rhs, self.rel_tol, self.max_iter,
-                       speculate=self.speculate)
-        self.vcycles -= rep.speculative_applies
+                       speculate=self.speculate, graphs=gi, owns_output=True)
+        if gi is not None:
+            self.vcycles += rep.iterations  # the in-graph P^-1 applications (the final one counted itself)
+        else:
+            self.vcycles -= rep.speculative_applies
         if check:
             self.precond.check_finite()
         u_next = u_n.clone()

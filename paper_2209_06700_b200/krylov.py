@@ -140,11 +140,134 @@ class _Ops:
             torch.div(w, h, out=out)
 
 
-def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, speculate=False):
+class GraphedIterations:
+    """Host-free GMRES iterations for small, host-bound problems (C1 / C3): fixed basis buffers and
+    ONE captured CUDA graph per iteration index j, holding w = A P^-1 v_j, the MGS column
+    (spk_mgs_column), v_{j+1} = w / h, the device Givens update of the least-squares residual
+    (spk_givens, krylov.py:84-87) and its copy into pinned host memory. A solve replays graph j, then
+    (speculatively) graph j + 1 before it waits for iteration j's residual, so the host only reads
+    two scalars per iteration; the final y is the reference's lstsq on the raw Hessenberg
+    (krylov.py:89, :106-110), copied to the host once. Graphs are captured on first use and reused by
+    every later solve of the same owner (same shapes, same buffers).
+
+    A and P must be capture-safe device callables returning fresh tensors (irk.StageSystem passes
+    its system operator and its un-graphed preconditioner body)."""
+
+    def __init__(self, A, P, shape, device, max_iter):
+        self.A, self.P, self.shape, self.device = A, P, tuple(shape), device
+        self.N = int(np.prod(self.shape))
+        self.max_iter = max_iter
+        self.cols = max_iter + 2
+        f64 = dict(dtype=torch.float64, device=device)
+        self.H = torch.zeros(self.cols * self.cols, **f64)
+        self.R = torch.zeros(self.cols * self.cols, **f64)
+        self.cs = torch.zeros(2 * self.cols, **f64)
+        self.g = torch.zeros(self.cols, **f64)
+        self.res = torch.zeros(self.cols, **f64)
+        self.scal = torch.zeros(4, **f64)
+        self.host = torch.zeros(2 * self.cols, dtype=torch.float64, pin_memory=True)
+        self.basis = [torch.zeros(self.N, **f64)]
+        self.ptrs = (_lib.ctypes.c_void_p * (max_iter + 2))()
+        self.ptrs[0] = self.basis[0].data_ptr()
+        self.graphs, self.outs = {}, {}
+        self.events = [torch.cuda.Event() for _ in range(self.cols)]
+        self.ctx = _ctx()
+        self.st = None
+        self._warm()
+
+    def _warm(self):
+        """one un-captured pass of every piece (lazy allocations, kernel attributes)"""
+        st = stream_ptr(self.device)
+        w = self.A(self.P(self.basis[0].reshape(self.shape))).reshape(-1).contiguous()
+        tmp = torch.zeros_like(self.basis[0])
+        _lib.call("spk_mgs_column", self.ctx, self.N, 0, _lib.ctypes.addressof(self.ptrs), ptr(w), ptr(self.R),
+                  ptr(tmp), st)
+        _lib.call("spk_mgs", self.ctx, self.N, ptr(w), None, None, None, ptr(self.scal), st)
+        _lib.call("spk_givens", ptr(self.R), ptr(self.R[self.cols:]), ptr(self.cs), ptr(self.g), ptr(self.res), 0, st)
+        torch.cuda.synchronize()
+
+    def hptr(self, i, j):
+        return self.H.data_ptr() + 8 * (j * self.cols + i)
+
+    def _body(self, j):
+        st = stream_ptr(self.device)
+        w = self.A(self.P(self.basis[j].reshape(self.shape))).reshape(-1)
+        if not w.is_contiguous():
+            w = w.contiguous()
+        _lib.call("spk_mgs_column", self.ctx, self.N, j, _lib.ctypes.addressof(self.ptrs), ptr(w), self.hptr(0, j),
+                  ptr(self.basis[j + 1]), st)
+        _lib.call("spk_givens", self.hptr(0, j), self.R.data_ptr() + 8 * j * self.cols, ptr(self.cs), ptr(self.g),
+                  self.res.data_ptr() + 8 * j, j, st)
+        self.host[2 * j : 2 * j + 1].copy_(self.res[j : j + 1], non_blocking=True)
+        self.host[2 * j + 1 : 2 * j + 2].copy_(self.H[j * self.cols + j + 1 : j * self.cols + j + 2], non_blocking=True)
+        return w
+
+    def launch(self, j):
+        if j + 1 >= len(self.basis):
+            self.basis.append(torch.zeros(self.N, dtype=torch.float64, device=self.device))
+            self.ptrs[j + 1] = self.basis[j + 1].data_ptr()
+        g = self.graphs.get(j)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.outs[j] = self._body(j)
+            self.graphs[j] = g
+        g.replay()
+        self.events[j].record()
+
+    def solve(self, b, rel_tol, report):
+        """GMRES on the device-resident (N,) rhs b; returns (k, happy) with basis / H filled."""
+        st = stream_ptr(self.device)
+        nb = self.scal.data_ptr()
+        _lib.call("spk_mgs", self.ctx, self.N, ptr(b), None, None, None, nb, st)
+        beta = float(self.scal[0].item())
+        report.residual_history.append(beta)
+        if beta == 0.0:
+            return 0, False, beta
+        _lib.call("spk_scale_div", self.N, ptr(b), nb, ptr(self.basis[0]), st)
+        self.g.zero_()
+        self.g[0:1].copy_(self.scal[0:1])
+        target = rel_tol * beta
+        k, happy, launched = 0, False, -1
+        self.launch(0)
+        launched = 0
+        hist = report.residual_history
+        for j in range(self.max_iter):
+            likely_last = len(hist) >= 2 and hist[-2] > 0 and hist[-1] * (hist[-1] / hist[-2]) <= target
+            if j + 1 < self.max_iter and launched == j and not likely_last:
+                self.launch(j + 1)
+                launched = j + 1
+            self.events[j].synchronize()
+            res, hsub = float(self.host[2 * j]), float(self.host[2 * j + 1])
+            if not (np.isfinite(res) and np.isfinite(hsub)):
+                raise NumericalFailureError("non-finite value in GMRES operator output")
+            k = j + 1
+            happy = abs(hsub) < BREAKDOWN_TOL
+            hist.append(res)
+            if happy or res <= target:
+                report.speculative_applies = 1 if launched > j else 0
+                break
+            if launched == j and j + 1 < self.max_iter:
+                self.launch(j + 1)
+                launched = j + 1
+        return k, happy, beta
+
+    def hessenberg(self, k):
+        Hc = self.H[: k * self.cols].reshape(k, self.cols)[:, : k + 1].cpu().numpy()
+        return Hc.T.copy()  # (k+1, k): column j = H[0..k, j]
+
+
+def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, speculate=False, graphs=None,
+          owns_output=False):
     """Solve A x = rhs with right preconditioning A P^{-1} y = rhs, x = P^{-1} y.
 
     rhs: torch CUDA tensor (device path) or numpy array (bridged). Returns (x, KrylovReport) with x in
     the container type of rhs.
+
+    graphs: a GraphedIterations of the caller (device path, real field): the iterations run as replayed
+    per-iteration CUDA graphs with the residual test on the device (see GraphedIterations).
+    owns_output: apply_A returns a fresh tensor per call, so its output is orthogonalised in place
+    (no defensive copy).
 
     speculate (device path): enqueue iteration j+1's A P^{-1} v_{j+1} before waiting for iteration j's
     Hessenberg column, so the host least-squares solve and the next launches overlap device work
@@ -182,6 +305,8 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
         return x.cpu().numpy() if host else x
 
     report = KrylovReport()
+    if graphs is not None and not host and not complex_:
+        return _gmres_graphed(graphs, A, P, b, n, shape, rel_tol, report, ops, out_of, device)
     beta_ptr = ops.hptr(0, max_iter + 1)  # scratch slot outside the used columns
     ops.norm_into(b, beta_ptr)
     beta = float(ops.col(max_iter + 1, 1)[0].real)
@@ -208,7 +333,9 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
     # real device path: one C call per MGS column (the j+2 fused sweeps and v_{j+1} = w / h)
     basis_ptrs = (_lib.ctypes.c_void_p * (max_iter + 1))() if not complex_ else None
     for j in range(max_iter):
-        w = w_next if w_next is not None else A(P(basis[j])).clone()
+        w = w_next if w_next is not None else A(P(basis[j]))
+        if w_next is None and not owns_output:
+            w = w.clone()
         w_next = None
         vcol = None
         if not complex_:
@@ -232,7 +359,9 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
             col_host[: j + 2].copy_(ops.H[j * ops.cols : j * ops.cols + j + 2], non_blocking=True)
             col_ev.record()
             vnext = vcol
-            w_next = A(P(vnext)).clone()
+            w_next = A(P(vnext))
+            if not owns_output:
+                w_next = w_next.clone()
             col_ev.synchronize()
             col = col_host[: j + 2].numpy().copy()
         else:
@@ -268,7 +397,9 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
         tbl = torch.tensor([v.data_ptr() for v in basis[:k]], dtype=torch.int64, device=device)
         _lib.call("spk_lincomb", n, k, tbl.data_ptr(), ptr(yd), ptr(z), ops.st)
     x = P(z).clone()
-    r = A(x).clone()
+    r = A(x)
+    if not owns_output:
+        r = r.clone()
     # ||b - A x|| : r -= 1 * b, then the norm (fused)
     one = ops.scal.data_ptr()
     res_ptr = ops.hptr(1, max_iter + 1)
@@ -281,6 +412,37 @@ def gmres(apply_A, apply_Pinv, rhs, rel_tol=1e-12, max_iter=200, dtype=None, spe
     report.iterations = k
     report.reduction_achieved = true_res / beta
     report.converged = happy or true_res <= target * (1.0 + 1e-9) or report.residual_history[-1] <= target
-    if not bool(torch.isfinite(x).all().item()):
+    if not np.isfinite(true_res):  # a non-finite x reaches ||b - A x|| (A is the identity on boundary rows)
+        raise NumericalFailureError("non-finite GMRES solution")
+    return out_of(x), report
+
+
+def _gmres_graphed(gi, A, P, b, n, shape, rel_tol, report, ops, out_of, device):
+    """Device-resident iterations (GraphedIterations), then the reference's final update: y from
+    lstsq on the raw Hessenberg (krylov.py:89), z = sum_i y_i v_i, x = P^-1 z, true residual."""
+    k, happy, beta = gi.solve(b, rel_tol, report)
+    if beta == 0.0:
+        report.converged = True
+        report.reduction_achieved = 0.0
+        return out_of(torch.zeros_like(b)), report
+    Hk = gi.hessenberg(k)
+    g = np.zeros(k + 1)
+    g[0] = beta
+    y, _ = _solve_hessenberg(Hk, g)
+    yd = torch.from_numpy(np.ascontiguousarray(y[:k].astype(np.float64))).to(device)
+    tbl = torch.tensor([v.data_ptr() for v in gi.basis[:k]], dtype=torch.int64, device=device)
+    z = torch.empty_like(b)
+    _lib.call("spk_lincomb", n, k, tbl.data_ptr(), ptr(yd), ptr(z), ops.st)
+    x = P(z).clone()
+    r = A(x)
+    one = ops.scal.data_ptr()
+    res_ptr = ops.hptr(1, gi.max_iter + 1)
+    _lib.call("spk_mgs", ops.ctx, n, ptr(r), ptr(b), one, None, res_ptr, ops.st)
+    true_res = float(ops.H[(gi.max_iter + 1) * ops.cols + 1].item())
+    target = rel_tol * beta
+    report.iterations = k
+    report.reduction_achieved = true_res / beta
+    report.converged = happy or true_res <= target * (1.0 + 1e-9) or report.residual_history[-1] <= target
+    if not np.isfinite(true_res):
         raise NumericalFailureError("non-finite GMRES solution")
     return out_of(x), report

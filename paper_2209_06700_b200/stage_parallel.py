@@ -323,7 +323,7 @@ class DistKrylov:
             w.sub_(Hd[hp] * v_prev)
         wo = self._own(w)
         c = self._own(v_cur) if v_cur is not None else wo
-        torch.sum(c * wo, out=Hd[out])
+        Hd[out : out + 1].copy_(torch.sum(c * wo).reshape(1))
 
     def _solve_device(self, A, P, b, rel_tol, max_iter):
         if self.owned is None and self.ctx is None:

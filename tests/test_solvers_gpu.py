@@ -153,6 +153,29 @@ def test_config1_steps_match_oracle(cuda):
     assert err < 1e-4
 
 
+@pytest.mark.parametrize("dim,L,k,Q", [(2, 4, 2, 2), (3, 3, 2, 3)])
+def test_graphed_iterations_match_host_iterations(cuda, dim, L, k, Q):
+    """GMRES iterations as replayed per-iteration CUDA graphs with the device Givens residual
+    (krylov.GraphedIterations) vs the host-driven loop with lstsq every iteration (krylov.py:84-87):
+    same iteration counts and V-cycle counts, solutions to 1e-12, over several steps (graph reuse)."""
+    tab = ref_radau(Q)
+    cfg = VCycleConfig(smoother_degree=3)
+    h = build_hierarchy(dim, L, k)
+    a = StageSystem(h, Q, 0.02, config=cfg, tableau=tab)
+    b = StageSystem(h, Q, 0.02, config=cfg, tableau=tab)
+    b.graph_iterations = False
+    assert a.graph_iterations
+    ua, ub = a.initial_condition(), b.initial_condition()
+    for s in range(3):
+        ua, ra = a.step(s * 0.02, ua)
+        ub, rb = b.step(s * 0.02, ub)
+        assert ra.iterations == rb.iterations and ra.vcycles_per_stage == rb.vcycles_per_stage == ra.iterations + 1
+        assert rel(ua.cpu().numpy(), ub.cpu().numpy()) < 1e-12
+        hs_a, hs_b = np.array(ra.residual_history), np.array(rb.residual_history)
+        assert np.allclose(hs_a, hs_b, rtol=1e-8, atol=1e-14 * hs_b[0])
+    assert len(a._gi.graphs) >= ra.iterations
+
+
 def test_config3_like_steps_match_oracle(cuda):
     """C3 settings (Q2, Radau Q=3, tau=0.01, Chebyshev degree 3) on a 8^3 mesh, 3 steps."""
     h, o = build_hierarchy(3, 3, 2), Hierarchy(3, 3, 2)

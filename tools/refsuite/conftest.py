@@ -5,11 +5,9 @@ through the device path (numpy arrays in, numpy arrays out: INTEGRATION.md §1).
 
 Run: python tools/refsuite/run.py <reference pkg/tests dir> (see tools/refsuite/run.py)."""
 
-import os
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, REPO)
+# run.py puts the repository on PYTHONPATH (this file is copied into a scratch directory)
 
 import paper_2209_06700_b200 as _pkg  # noqa: E402
 from paper_2209_06700_b200 import errors, fem, krylov, multigrid, tableau  # noqa: E402

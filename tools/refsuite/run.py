@@ -30,7 +30,9 @@ def main():
             shutil.copy(f, work)
         cmd = [sys.executable, "-m", "pytest", "-p", "no:cacheprovider", "-q", "-rfEx", work,
                "--deselect", os.path.join(work, KNOWN_REFERENCE_FAILURE), *extra]
-        r = subprocess.run(cmd, cwd=work)
+        repo = os.path.dirname(os.path.dirname(HERE))
+        env = dict(os.environ, PYTHONPATH=repo + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        r = subprocess.run(cmd, cwd=work, env=env)
         print(f"reference tests: {[os.path.basename(f) for f in names]}; deselected (fails on the reference "
               f"itself): {KNOWN_REFERENCE_FAILURE}")
         return r.returncode
