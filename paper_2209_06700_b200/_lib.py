@@ -103,7 +103,10 @@ def load():
             f"libspk not built ({LIB_PATH} missing): run `python -c 'import __graft_entry__ as g; g.build()'`"
         )
     lib = ctypes.CDLL(LIB_PATH)
+    lax = os.environ.get("SPK_LIB_LAX") == "1"  # A/B of older library builds (tools/ab_apply.py)
     for name, (args, res) in _SIGS.items():
+        if lax and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

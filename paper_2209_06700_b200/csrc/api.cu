@@ -7,9 +7,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/spk.h"
 #include "spk_internal.cuh"
 #include "spk_vecops.cuh"
+
+namespace {
+// NVTX range per C-ABI entry point (free when no profiler is attached): the timeline of a step
+// (ncu / nsight) shows which reference operation each kernel serves
+struct SpkRange {
+  explicit SpkRange(const char* name) { nvtxRangePushA(name); }
+  ~SpkRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define SPK_RANGE(name) SpkRange spk_range_guard_(name)
 
 struct spk_ctx {
   int dim = 0, max_level = 0, K = 0;
@@ -523,6 +535,7 @@ int spk_set_cheb_split(spk_ctx* c, long long min_block_dofs) {
 
 int spk_stage_apply(spk_ctx* c, int level, int Q, const double* DM, const double* DK, int constrained,
                     const double* u, long long su, double* v, long long sv, void* stream) {
+  SPK_RANGE("spk_stage_apply");
   if (int rc = check_level(c, level)) return rc;
   if (Q < 1 || Q > SPK_QMAX)
     return fail(SPK_EUNSUPPORTED, "fused stage operator supports Q in [1, 4], got " + std::to_string(Q));
@@ -540,6 +553,7 @@ int spk_stage_apply(spk_ctx* c, int level, int Q, const double* DM, const double
 int spk_stage_apply_slab(spk_ctx* c, int level, int Q, const double* DM, const double* DK,
                          const double* u, long long su, double* v, long long sv, int x_elems,
                          int ex_begin, int ex_end, int store_last, void* stream) {
+  SPK_RANGE("spk_stage_apply_slab");
   if (int rc = check_level(c, level)) return rc;
   if (c->dim != 3) return fail(SPK_ECONFIG, "slab windows need a 3D hierarchy");
   if (Q < 1 || Q > SPK_QMAX)
@@ -563,6 +577,7 @@ int spk_stage_apply_slab(spk_ctx* c, int level, int Q, const double* DM, const d
 int spk_block_apply(spk_ctx* c, int level, int nblk, const double* lams, int lam_uniform, double tau,
                     int constrained, const double* u, long long su, double* v, long long sv,
                     void* stream) {
+  SPK_RANGE("spk_block_apply");
   if (int rc = check_level(c, level)) return rc;
   if (nblk < 1) return SPK_OK;
   SpkApplyArgs a = base_args(c, level);
@@ -573,6 +588,7 @@ int spk_block_apply(spk_ctx* c, int level, int nblk, const double* lams, int lam
 
 int spk_pair_apply(spk_ctx* c, int level, double re, double im, double tau, int constrained,
                    const double* u, double* v, void* stream) {
+  SPK_RANGE("spk_pair_apply");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs a = base_args(c, level);
@@ -585,6 +601,7 @@ int spk_pair_apply(spk_ctx* c, int level, double re, double im, double tau, int 
 
 int spk_residual(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* x,
                  const double* b, double* r, double* d_out, const double* c2s, void* stream) {
+  SPK_RANGE("spk_residual");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs a = base_args(c, level);
@@ -595,6 +612,7 @@ int spk_residual(spk_ctx* c, int level, int nblk, const double* lams, double tau
 
 int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* cs,
                   const double* b, double* r, double* x, double* d, void* stream) {
+  SPK_RANGE("spk_cheb_init");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
@@ -613,6 +631,7 @@ int spk_cheb_init(spk_ctx* c, int level, int nblk, const double* lams, double ta
 
 int spk_cheb_start(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* thetas,
                    const double* b, double* d, void* stream) {
+  SPK_RANGE("spk_cheb_start");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   for (int b0 = 0; b0 < nblk; b0 += SPK_BMAX) {
@@ -632,6 +651,7 @@ int spk_cheb_start(spk_ctx* c, int level, int nblk, const double* lams, double t
 int spk_cheb_first_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
                         const double* c2s, const double* b, const double* d_in, double* r, double* x,
                         double* d_out, int final_step, int* nan_flag, void* stream) {
+  SPK_RANGE("spk_cheb_first_step");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs ap = base_args(c, level);
@@ -667,6 +687,7 @@ int spk_cheb_split(spk_ctx* c, int level, int nblk) {
 int spk_cheb_step(spk_ctx* c, int level, int nblk, const double* lams, double tau, const double* c1s,
                   const double* c2s, const double* d_in, double* r, double* x, double* d_out,
                   int final_step, int* nan_flag, void* stream) {
+  SPK_RANGE("spk_cheb_step");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   if (cheb_split(c, level, nblk)) {
@@ -747,6 +768,7 @@ int spk_pair_cheb_step(spk_ctx* c, int level, double re, double im, double tau, 
 
 int spk_dinv_norm(spk_ctx* c, int level, int pair, double lam_or_re, double im, double tau,
                   const double* u, double* w, double* norm_dev, void* stream) {
+  SPK_RANGE("spk_dinv_norm");
   if (int rc = check_level(c, level)) return rc;
   const long long n = c->dims[level].n;
   SpkApplyArgs a = base_args(c, level);
@@ -776,6 +798,7 @@ int spk_dinv_norm(spk_ctx* c, int level, int pair, double lam_or_re, double im, 
 
 int spk_transfer(spk_ctx* c, int level, int nblk, int prolong, const double* in, double* out,
                  double* scratch, int accumulate, int mask, void* stream) {
+  SPK_RANGE("spk_transfer");
   if (int rc = check_level(c, level)) return rc;
   if (level < 1) return fail(SPK_ECONFIG, "transfer needs level >= 1");
   const SpkDims gf = c->dims[level], gc = c->dims[level - 1];
@@ -856,6 +879,7 @@ int spk_axpy_flag(long long total, double* x, const double* d, int* flag, void* 
 int spk_combine(spk_ctx* c, int mask_level, long long n, int nin, int nout, const double* D,
                 const double* in, long long sin, double* out, long long sout, int accumulate,
                 void* stream) {
+  SPK_RANGE("spk_combine");
   if (nin < 1 || nout < 1 || nin > SPK_CMAX || nout > SPK_CMAX)
     return fail(SPK_EUNSUPPORTED, "combine supports up to 18 rows/columns");
   SpkCombineArgs a;
@@ -877,6 +901,7 @@ int spk_combine(spk_ctx* c, int mask_level, long long n, int nin, int nout, cons
 
 int spk_peer_combine(long long n, int nin, const double* const* in_rows, int nout, const double* D,
                      double* out, long long sout, int accumulate, void* stream) {
+  SPK_RANGE("spk_peer_combine");
   if (nin < 1 || nout < 1 || nin > SPK_CMAX || nout > SPK_CMAX)
     return fail(SPK_EUNSUPPORTED, "peer combine supports up to 18 rows/columns");
   SpkCombineArgs a;
@@ -1007,6 +1032,7 @@ int spk_coarse_vcycle_level(spk_ctx* c) {
 
 int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double tau, int deg, const double* coef,
                       const double* cinv, const double* b, double* x, double* scratch, int* flags, void* stream) {
+  SPK_RANGE("spk_coarse_vcycle");
   if (!c) return fail(SPK_ECONFIG, "null context");
   if (lc < 1 || lc > spk_coarse_vcycle_level(c)) return fail(SPK_ECONFIG, "coarse_vcycle: level not fusable");
   if (nblk < 1 || nblk > SPK_BMAX || deg < 1 || deg > 8) return fail(SPK_ECONFIG, "coarse_vcycle: bad sizes");
@@ -1030,6 +1056,7 @@ int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double t
 
 int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, double* w, double* hcol,
                    double* v_next, void* stream) {
+  SPK_RANGE("spk_mgs_column");
   // column j of modified Gram-Schmidt (krylov.py:74-82) as one call: j+2 fused sweeps, then
   // v_{j+1} = w / h_{j+1,j}; hcol points at H[0, j] (H[i, j] = hcol[i], device-resident)
   if (!c) return fail(SPK_ECONFIG, "null context");
@@ -1076,6 +1103,7 @@ int spk_outer3(spk_ctx* c, int level, const double* g1_dev, double* out, void* s
 
 int spk_rhs(spk_ctx* c, int level, int Q, const double* g1_dev, const double* T, const double* Ainv,
             const double* ku, double* out, void* stream) {
+  SPK_RANGE("spk_rhs");
   if (int rc = check_level(c, level)) return rc;
   if (Q < 1 || Q > SPK_CMAX) return fail(SPK_EUNSUPPORTED, "rhs: bad Q");
   SpkRhsArgs a;

@@ -55,13 +55,17 @@ template <int K, int Q> struct Geo {
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
   static constexpr int TZp = TZ | 1;
-  static constexpr int U_SZ = Q * NYin * NZp;          // one plane buffer
+  // bulk-copy layout (interior tiles, SPK_BULK_LOAD): 16-byte aligned rows of NZb doubles, each holding
+  // its NZin values at a per-row offset of 0 or 1 (the global row start rounded down to 16 bytes)
+  static constexpr int NZb = (NZin + 2) & ~1;
+  static constexpr int U_SZ = Q * NYin * (NZp > NZb ? NZp : NZb);  // one plane buffer
+  static constexpr int BROWS = Q * NYin;                           // bulk copies per plane
   static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
   static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
   // Jacobi table: one entry per (x,y,z) node class ((K+1)^3) and block (block mode) / (A, B) (pair)
   static constexpr int DT_STRIDE = (Q > 2 ? Q : 2);
   static constexpr int DT_SZ = (K + 1) * (K + 1) * (K + 1) * DT_STRIDE;
-  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ + DT_SZ;
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ + DT_SZ + 2;  // + 2 mbarriers
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
 #ifdef SPK_ZS
@@ -144,6 +148,46 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int 
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+// ---- Blackwell bulk-async copies (the TMA engine's non-tensor path: UBLKCP) completing on an
+//      mbarrier transaction count (SYNCS) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SPK_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SPK_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Measured on B200 (tools/ab_apply.py, profiles/r02_k1_ab.txt) and REJECTED as the default: one
+// 176-byte bulk copy per row (63 per plane at C2, issued by warp 0) through the async copy engine
+// ran C2 at 711 us against 428 us for the per-node cp.async path -- the row copies serialise in the
+// engine, and the 16-byte aligned rows cost the Z-phase its odd-pitch conflict-free reads. The n_ax =
+// k 2^l + 1 layout (odd row stride, 2056 bytes at C2) rules out 2D/3D tensor maps (TMA needs
+// 16-byte multiple strides), so a plane cannot be one TMA box. Kept behind -DSPK_BULK_LOAD=1.
+#ifndef SPK_BULK_LOAD
+#define SPK_BULK_LOAD 0
+#endif
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // assembled 1D reference diagonal at node i of an axis with E elements (E == 0: degenerate axis)
@@ -414,6 +458,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   double* ABs = Us + 2 * G::U_SZ;       // [2][Q][NYin][TZp] of (A, B) pairs (16-byte accesses)
   double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][Q][TY][TZp] of (MA, C) pairs
   double* dtab = MCs + 2 * G::NBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
+  unsigned long long* ubar = reinterpret_cast<unsigned long long*>(dtab + G::DT_SZ);  // plane-buffer mbarriers
+  // interior tiles load their planes with bulk-async copies (one per row, issued by warp 0) that
+  // complete on ubar[slot]; every other tile keeps the per-node cp.async path with zero-fill
+  constexpr bool BULK = FULL && SPK_BULK_LOAD;
 
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
@@ -507,7 +555,43 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
+  // bulk descriptors: lane l of warp 0 copies rows l, l + 32, ...; per-row source element index
+  // (plane 0) and the parity of the row start for the Z-phase offset
+  constexpr int BRI = (G::BROWS + 31) / 32;
+  long long bsrc[BULK ? BRI : 1];
+  unsigned bpar0 = 0u;  // bit i: row start index parity at plane 0 (row = zoff of Z item i)
+  const unsigned podd = static_cast<unsigned>(plane_stride & 1);
+  if constexpr (BULK) {
+#pragma unroll
+    for (int i = 0; i < BRI; ++i) {
+      const int r = min(tid % 32 + 32 * i, G::BROWS - 1);
+      const int q = r / NYin, yy = r - q * NYin;
+      bsrc[i] = (long long)q * a.su + (long long)(y_lo - K + yy) * g.nz + (z_lo - K);
+    }
+  }
+  auto load_plane_bulk = [&](int x, auto BUF) {
+    const unsigned buf = parity_of(BUF);
+    if (tid >= 32) return;
+    double* Ub = Us + buf * G::U_SZ;
+    if (tid == 0) mbar_arrive_expect_tx(&ubar[buf], G::BROWS * G::NZb * 8);
+    __syncwarp();
+    fence_proxy_async_smem();  // the buffer's previous generic-proxy readers are ordered before
+#pragma unroll
+    for (int i = 0; i < BRI; ++i) {
+      const int r = tid + 32 * i;
+      if (r < G::BROWS) {
+        const double* src = u + bsrc[i] + (long long)x * plane_stride;
+        const uintptr_t al = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+        bulk_g2s(Ub + r * G::NZb, reinterpret_cast<const void*>(al), G::NZb * 8, &ubar[buf]);
+      }
+    }
+  };
+
   auto load_plane = [&](int x, auto BUF) {
+    if constexpr (BULK) {
+      load_plane_bulk(x, BUF);
+      return;
+    }
     const unsigned buf = parity_of(BUF);
     const unsigned long long base =
         reinterpret_cast<unsigned long long>(u) + (unsigned long long)x * (unsigned long long)plane_stride * 8ull;
@@ -564,6 +648,15 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
       }
     }
   }
+  if constexpr (BULK) {
+#pragma unroll
+    for (int i = 0; i < G::ZIT; ++i) {
+      const int q = zoff[i] / NYin, yy = zoff[i] - q * NYin;
+      const long long e0 = (long long)q * a.su + (long long)(y_lo - K + yy) * g.nz + (z_lo - K);
+      const uintptr_t addr = reinterpret_cast<uintptr_t>(u + e0);
+      bpar0 |= static_cast<unsigned>((addr >> 3) & 1u) << i;
+    }
+  }
   // Y items: (q, z, segment of YS elements); lanes run along z
   int yoff[G::YIT], yeb[G::YIT];
 #pragma unroll
@@ -585,14 +678,17 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   }
 
   // ---------------- Z-phase: A = Mz u, B = Kz u ----------------
-  auto zphase = [&](auto PB) {
+  auto zphase = [&](auto PB, int xp) {
     const int ub = parity_of(PB), ab = ub;
     const double* Ub = Us + ub * G::U_SZ;
     double2* AB = reinterpret_cast<double2*>(ABs + ab * 2 * G::AB_SZ);
+    // constrained: the x-boundary planes are zero (bulk copies cannot zero-fill: their Z outputs are)
+    const bool xzero = BULK && a.constrained && (xp + g.x0 == 0 || xp + g.x0 == g.nxg - 1);
+    const unsigned pflip = BULK ? ((static_cast<unsigned>(xp) & podd) ? ~0u : 0u) : 0u;
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
       if (zeb[i] >= nez) continue;
-      const double* row = Ub + zoff[i] * NZp;
+      const double* row = BULK ? Ub + zoff[i] * G::NZb + (((bpar0 ^ pflip) >> i) & 1u) : Ub + zoff[i] * NZp;
       double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
       double L[K + 1], R[K + 1];
@@ -609,6 +705,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
           const double wl = (FULL || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
           double oa[K], ob[K];
           elem2<K>(cf, L, R, wl, wr, oa, ob);
+          if (BULK && xzero) {
+#pragma unroll
+            for (int r = 0; r < K; ++r) oa[r] = ob[r] = 0.0;
+          }
 #pragma unroll
           for (int r = 0; r < K; ++r) {
             const int zl = K * e + r;
@@ -814,13 +914,25 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // unrolled by two so every buffer address is a compile-time offset.
   auto interval = [&](auto P, int t) {
     constexpr int p = decltype(P)::value;  // == t & 1
-    cp_async_wait_all();
+    if constexpr (BULK) {
+      if (t < nplanes) mbar_wait(&ubar[p], static_cast<unsigned>(t >> 1) & 1u);
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();
     if (t + 1 < nplanes) load_plane(xs + t + 1, IC<1 - p>{});
-    if (t < nplanes) zphase(IC<p>{});
+    if (t < nplanes) zphase(IC<p>{}, xs + t);
     if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{});
     if (t >= 2) xphase(xs + t - 2, IC<p>{});
   };
+  if constexpr (BULK) {
+    if (tid == 0) {
+      mbar_init(&ubar[0], 1);
+      mbar_init(&ubar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
   spk_pdl_wait();  // everything above reads parameters / constants only
   load_plane(xs, IC<0>{});
   // unroll the plane loop by two (compile-time buffer offsets); measured on B200 to help every
@@ -835,10 +947,14 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   } else {  // one copy of the interval with runtime buffer parity (smaller code)
     for (int t = 0; t < nplanes + 2; ++t) {
       const int p = t & 1;
-      cp_async_wait_all();
+      if constexpr (BULK) {
+        if (t < nplanes) mbar_wait(&ubar[p], static_cast<unsigned>(t >> 1) & 1u);
+      } else {
+        cp_async_wait_all();
+      }
       __syncthreads();
       if (t + 1 < nplanes) load_plane(xs + t + 1, 1 - p);
-      if (t < nplanes) zphase(p);
+      if (t < nplanes) zphase(p, xs + t);
       if (t >= 1 && t - 1 < nplanes) yphase(1 - p);
       if (t >= 2) xphase(xs + t - 2, p);
     }
@@ -876,9 +992,11 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB 
     // element of the tile real (ey0 >= 1, ey0 + TYE <= Ey), and away from the constrained boundary
     const SpkDims& g = a.g;
     const int ez0 = blockIdx.x * G::TZE, ey0 = blockIdx.y * G::TYE;
-    const int lo = a.constrained ? 2 : 1, hi = a.constrained ? 1 : 0;
+    // (bulk loads: one more element on the high z side, since a row copy may read one double past
+    // the row's last loaded value; no virtual x-split)
+    const int lo = a.constrained ? 2 : 1, hi = (a.constrained || SPK_BULK_LOAD) ? 1 : 0;
     const bool full = g.Ey > 0 && g.Ez > 0 && g.Ex > 0 && ey0 >= lo && ez0 >= lo && ey0 + G::TYE + hi <= g.Ey &&
-                      ez0 + G::TZE + hi <= g.Ez;
+                      ez0 + G::TZE + hi <= g.Ez && !(SPK_BULK_LOAD && BLOCK && a.vplanes != 0);
     if (full) {
       stage_apply_body<K, Q, BLOCK, EPI, true>(a, smem);
       return;

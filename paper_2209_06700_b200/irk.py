@@ -143,11 +143,17 @@ class StageSystem:
 
     def step(self, t_n, u_n, check=True):
         """u_{n+1} for device u_n (n,), and the SolveReport."""
+        nvtx = torch.cuda.nvtx
+        nvtx.range_push("radau_step")
+        nvtx.range_push("assemble_rhs")
         rhs = self.assemble_rhs(t_n, u_n)
+        nvtx.range_pop()
         v0 = self.vcycles
         gi = self._graphed_iterations()
+        nvtx.range_push("gmres")
         k, rep = gmres(self.apply_system_operator, self.apply_preconditioner, rhs, self.rel_tol, self.max_iter,
                        speculate=self.speculate, graphs=gi, owns_output=True)
+        nvtx.range_pop()
         if gi is not None:
             self.vcycles += rep.iterations  # the in-graph P^-1 applications (the final one counted itself)
         else:
@@ -157,6 +163,7 @@ class StageSystem:
         u_next = u_n.clone()
         _lib.call("spk_update", self.n, self.Q, ptr(k), ptr(self._bw), self.tau, ptr(u_next),
                   stream_ptr(self.h.device))
+        nvtx.range_pop()
         report = SolveReport(iterations=rep.iterations, vcycles_per_stage=self.vcycles - v0,
                              vcycles_total=self.Q * (self.vcycles - v0),
                              residual_history=rep.residual_history, converged=rep.converged)

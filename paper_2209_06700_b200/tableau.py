@@ -126,8 +126,30 @@ def radau_iia(Q):
         for j in range(Q):
             A[i, j] = float(np.dot(ws, _lagrange_basis(c, j, s)))
     b = A[Q - 1].copy()
-    Ainv = np.linalg.inv(A)
+    Ainv = _exact_inverse(A)
     return ButcherTableau(Q=Q, A=A, b=b, c=c, Ainv=Ainv)
+
+
+def _exact_inverse(A):
+    """inv(A) of the float64 matrix A computed exactly (rational Gauss-Jordan with partial
+    pivoting) and rounded once: the correctly rounded inverse. The LU factor's eigenbasis is
+    ill-conditioned for Q >= 8, and a LAPACK inverse's last-bit errors there push the reference's
+    spectral reconstruction check (test_tableau.py:138-146) over its 1e-10 bound."""
+    n = A.shape[0]
+    M = [[Fraction(float(A[i, j])) for j in range(n)] + [Fraction(int(i == j)) for j in range(n)]
+         for i in range(n)]
+    for col in range(n):
+        piv = max(range(col, n), key=lambda r: abs(M[r][col]))
+        if M[piv][col] == 0:
+            raise FactorizationError(col)
+        M[col], M[piv] = M[piv], M[col]
+        inv_p = 1 / M[col][col]
+        M[col] = [v * inv_p for v in M[col]]
+        for r in range(n):
+            if r != col and M[r][col] != 0:
+                f = M[r][col]
+                M[r] = [x - f * y for x, y in zip(M[r], M[col])]
+    return np.array([[float(M[i][n + j]) for j in range(n)] for i in range(n)])
 
 
 def crout_lu(Ainv):

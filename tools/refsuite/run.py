@@ -28,8 +28,8 @@ def main():
         names = sorted(glob.glob(os.path.join(src, "test_*.py")))
         for f in names:
             shutil.copy(f, work)
-        cmd = [sys.executable, "-m", "pytest", "-p", "no:cacheprovider", "-q", "-rfEx", work,
-               "--deselect", os.path.join(work, KNOWN_REFERENCE_FAILURE), *extra]
+        cmd = [sys.executable, "-m", "pytest", "-p", "no:cacheprovider", "-q", "-rfEx", ".",
+               "--deselect", KNOWN_REFERENCE_FAILURE, *extra]
         repo = os.path.dirname(os.path.dirname(HERE))
         env = dict(os.environ, PYTHONPATH=repo + os.pathsep + os.environ.get("PYTHONPATH", ""))
         r = subprocess.run(cmd, cwd=work, env=env)
