@@ -41,3 +41,28 @@ def like_input(t, template):
     if is_host(template):
         return t.detach().cpu().numpy()
     return t
+
+
+class capture_graph:
+    """torch.cuda.graph(g) with Python's garbage collector held off for the capture: a collected
+    object whose finaliser frees device memory (GridHierarchy -> spk_ctx_destroy -> cudaFree)
+    would otherwise invalidate the capture and abort the process."""
+
+    def __init__(self, graph):
+        import torch
+        self._ctx = torch.cuda.graph(graph)
+
+    def __enter__(self):
+        import gc
+        self._gc = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        return self._ctx.__enter__()
+
+    def __exit__(self, *exc):
+        import gc
+        try:
+            return self._ctx.__exit__(*exc)
+        finally:
+            if self._gc:
+                gc.enable()

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import ptr, stream_ptr
+from ._device import capture_graph, ptr, stream_ptr
 from .errors import StepFailureError
 from .irk import SolveReport, StageSystem
 from .krylov import gmres
@@ -61,7 +61,7 @@ class DirectComplexSystem(StageSystem):
                 fn(g_in)  # warm-up: configures kernels, allocates
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with capture_graph(g):
                     g_out = fn(g_in).clone()
                 ent = (g_in, g, g_out)
                 cache[key] = ent

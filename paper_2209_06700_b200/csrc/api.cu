@@ -1020,11 +1020,11 @@ int spk_sqrt_dev(double* x, int count, void* stream) {
 }
 
 int spk_coarse_vcycle_level(spk_ctx* c) {
-  if (!c || c->dim != 3) return -1;
+  if (!c || c->dim < 2) return -1;
   int best = -1;
   for (int l = 1; l <= c->max_level && l <= SPK_CV_LMAX; ++l) {
     if (!whole_level(c, l) || !whole_level(c, l - 1)) break;
-    if (spk_coarse_vcycle_smem(c->K, l) > SPK_CV_SMEM_MAX || c->dims[l].n > c->cv_max_nodes) break;
+    if (spk_coarse_vcycle_smem(c->K, l, c->dim) > SPK_CV_SMEM_MAX || c->dims[l].n > c->cv_max_nodes) break;
     best = l;
   }
   return best;
@@ -1038,11 +1038,11 @@ int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double t
   if (nblk < 1 || nblk > SPK_BMAX || deg < 1 || deg > 8) return fail(SPK_ECONFIG, "coarse_vcycle: bad sizes");
   SpkCoarseArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.lc = lc; a.nblk = nblk; a.deg = deg; a.tau = tau;
+  a.lc = lc; a.nblk = nblk; a.deg = deg; a.tau = tau; a.dim = c->dim;
   for (int i = 0; i < nblk; ++i) a.lam[i] = lams[i];
-  for (int l = 0; l <= lc; ++l) {
-    a.hd[l] = std::pow(c->h[l], 3);
-    a.hk[l] = c->h[l];
+  for (int l = 0; l <= lc; ++l) {  // M = h^d M_hat, K = h^(d-2) K_hat on the reference tables
+    a.hd[l] = std::pow(c->h[l], c->dim);
+    a.hk[l] = std::pow(c->h[l], c->dim - 2);
   }
   for (int f = 0; f <= 2 * c->K; ++f)
     for (int j = 0; j <= c->K; ++j) a.P[f * (SPK_KMAX + 1) + j] = c->P[f * (SPK_KMAX + 1) + j];

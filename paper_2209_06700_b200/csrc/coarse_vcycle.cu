@@ -1,5 +1,6 @@
-// Fused V-cycle on the coarsest levels of a whole-mesh 3D hierarchy (block family, direct coarse
-// solve), sm_100a, fp64.
+// Fused V-cycle on the coarsest levels of a whole-mesh 2D or 3D hierarchy (block family, direct
+// coarse solve), sm_100a, fp64. A 2D level is a 3D one with a single x plane (degenerate x axis: the
+// x factors of M and K are 1 and 0, the x sweeps of the operator and the transfers vanish).
 //
 // Below a few thousand nodes per block every kernel of the V-cycle (multigrid.py:110-140: Chebyshev
 // steps, residual, restriction, prolongation, the coarse solve) is a launch of a few microseconds
@@ -22,12 +23,14 @@ constexpr int CV_NT = 512;
 
 template <int K>
 struct CVLevel {
-  int m, n;  // nodes per axis, nodes
-  __device__ CVLevel(int l) : m((K << l) + 1), n(((K << l) + 1) * ((K << l) + 1) * ((K << l) + 1)) {}
+  int m, mx, n;  // nodes per axis (y, z), nodes along x (1 in 2D), nodes
+  __device__ CVLevel(int l, int dim)
+      : m((K << l) + 1), mx(dim == 3 ? (K << l) + 1 : 1), n(mx * ((K << l) + 1) * ((K << l) + 1)) {}
 };
 
-__device__ __forceinline__ bool cv_bnd(int x, int y, int z, int m) {
-  return x == 0 || x == m - 1 || y == 0 || y == m - 1 || z == 0 || z == m - 1;
+// boundary node; mx == 1: degenerate x axis (2D), no x boundary
+__device__ __forceinline__ bool cv_bnd(int x, int y, int z, int m, int mx) {
+  return (mx > 1 && (x == 0 || x == m - 1)) || y == 0 || y == m - 1 || z == 0 || z == m - 1;
 }
 
 // band-row class of node i on an axis of m nodes (Band<K>::cls with the whole-axis convention)
@@ -41,11 +44,11 @@ __device__ __forceinline__ int cv_cls(int i, int m) {
 // Jacobi inverse diagonal of the constrained block operator at (x, y, z): 1 on boundary rows,
 // else 1 / (lam' dm + tau' dk) with the Kronecker diagonal pieces (fem.py:172-187 association order)
 template <int K>
-__device__ __forceinline__ double cv_dinv(int x, int y, int z, int m, double lamp, double taup) {
-  if (cv_bnd(x, y, z, m)) return 1.0;
-  const int E = (m - 1) / K;
+__device__ __forceinline__ double cv_dinv(int x, int y, int z, int m, int nx, double lamp, double taup) {
+  if (cv_bnd(x, y, z, m, nx)) return 1.0;
+  const int E = (m - 1) / K, Ex = nx > 1 ? E : 0;
   double mx, kx, my, ky, mz, kz;
-  class_diag1<K>(axis_class<K>(x, m, E), E, mx, kx);
+  class_diag1<K>(axis_class<K>(x, nx, Ex), Ex, mx, kx);
   class_diag1<K>(axis_class<K>(y, m, E), E, my, ky);
   class_diag1<K>(axis_class<K>(z, m, E), E, mz, kz);
   const double dm = (mx * my) * mz;
@@ -54,6 +57,7 @@ __device__ __forceinline__ double cv_dinv(int x, int y, int z, int m, double lam
 }
 
 struct CVShared {
+  int dim;
   double* X[SPK_CV_LMAX + 1];
   double* B[SPK_CV_LMAX + 1];
   double* DI[SPK_CV_LMAX + 1];  // Jacobi inverse diagonal per level (computed once per launch)
@@ -67,8 +71,8 @@ struct CVShared {
 template <int K>
 __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, double lamp, double taup) {
   constexpr int W = 2 * K + 1;
-  const CVLevel<K> L(l);
-  const int m = L.m, n = L.n, mm = m * m;
+  const CVLevel<K> L(l, S.dim);
+  const int m = L.m, n = L.n, mm = m * m, mx = L.mx;
   const int* co = S.CO[l];
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // z: T0 = Mz u, T1 = Kz u
     const int cw = co[i], x = cw & 1023, y = (cw >> 10) & 1023, z = cw >> 20;
@@ -78,7 +82,7 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
     for (int d = 0; d < W; ++d) {
       const int zz = z + d - K;
       if (zz < 0 || zz >= m) continue;
-      const double uv = cv_bnd(x, y, zz, m) ? 0.0 : u[i + d - K];
+      const double uv = cv_bnd(x, y, zz, m, mx) ? 0.0 : u[i + d - K];
       a = fma(S.bm[c * W + d], uv, a);
       b = fma(S.bk[c * W + d], uv, b);
     }
@@ -105,8 +109,12 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // x: v = Mx p + Kx q ; boundary rows identity
     const int cw = co[i], x = cw & 1023, y = (cw >> 10) & 1023, z = cw >> 20;
-    if (cv_bnd(x, y, z, m)) {
+    if (cv_bnd(x, y, z, m, mx)) {
       v[i] = u[i];
+      continue;
+    }
+    if (mx == 1) {  // 2D: the degenerate x factors are Mx = 1, Kx = 0
+      v[i] = S.T2[i];
       continue;
     }
     const int c = cv_cls<K>(x, m);
@@ -159,21 +167,30 @@ __device__ __forceinline__ double cv_tv(const double* P, int prolong, int Nc, in
 template <int K>
 __device__ void cv_restrict(const CVShared& S, const double* P, int l) {
   const int mf = (K << l) + 1, mc = (K << (l - 1)) + 1, Nc = 1 << (l - 1);
-  for (int i = threadIdx.x; i < mf * mf * mc; i += CV_NT) {  // [xf][yf][zc]
+  const int mxf = S.dim == 3 ? mf : 1;
+  for (int i = threadIdx.x; i < mxf * mf * mc; i += CV_NT) {  // [xf][yf][zc]
     const int zc = i % mc, t = i / mc;
     S.T0[i] = cv_tv<K>(P, 0, Nc, zc, S.R + t * mf, 1);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < mf * mc * mc; i += CV_NT) {  // [xf][yc][zc]
+  for (int i = threadIdx.x; i < mxf * mc * mc; i += CV_NT) {  // [xf][yc][zc]
     const int zc = i % mc, t = i / mc, yc = t % mc, xf = t / mc;
     S.T1[i] = cv_tv<K>(P, 0, Nc, yc, S.T0 + xf * mf * mc + zc, mc);
   }
   __syncthreads();
   double* Bc = S.B[l - 1];
+  if (S.dim == 2) {  // no x sweep: mask the (yc, zc) result
+    for (int i = threadIdx.x; i < mc * mc; i += CV_NT) {
+      const int zc = i % mc, yc = i / mc;
+      Bc[i] = cv_bnd(0, yc, zc, mc, 1) ? 0.0 : S.T1[i];
+    }
+    __syncthreads();
+    return;
+  }
   for (int i = threadIdx.x; i < mc * mc * mc; i += CV_NT) {  // [xc][yc][zc], masked
     const int zc = i % mc, t = i / mc, yc = t % mc, xc = t / mc;
     const double val = cv_tv<K>(P, 0, Nc, xc, S.T1 + yc * mc + zc, mc * mc);
-    Bc[i] = cv_bnd(xc, yc, zc, mc) ? 0.0 : val;
+    Bc[i] = cv_bnd(xc, yc, zc, mc, mc) ? 0.0 : val;
   }
   __syncthreads();
 }
@@ -182,18 +199,24 @@ __device__ void cv_restrict(const CVShared& S, const double* P, int l) {
 template <int K>
 __device__ void cv_prolong(const CVShared& S, const double* P, int l) {
   const int mf = (K << l) + 1, mc = (K << (l - 1)) + 1, Nc = 1 << (l - 1);
+  const int mxc = S.dim == 3 ? mc : 1;
   const double* Xc = S.X[l - 1];
-  for (int i = threadIdx.x; i < mc * mc * mf; i += CV_NT) {  // [xc][yc][zf]
+  for (int i = threadIdx.x; i < mxc * mc * mf; i += CV_NT) {  // [xc][yc][zf]
     const int zf = i % mf, t = i / mf;
     S.T0[i] = cv_tv<K>(P, 1, Nc, zf, Xc + t * mc, 1);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < mc * mf * mf; i += CV_NT) {  // [xc][yf][zf]
+  for (int i = threadIdx.x; i < mxc * mf * mf; i += CV_NT) {  // [xc][yf][zf]
     const int zf = i % mf, t = i / mf, yf = t % mf, xc = t / mf;
     S.T1[i] = cv_tv<K>(P, 1, Nc, yf, S.T0 + xc * mc * mf + zf, mf);
   }
   __syncthreads();
   double* Xf = S.X[l];
+  if (S.dim == 2) {  // no x sweep
+    for (int i = threadIdx.x; i < mf * mf; i += CV_NT) Xf[i] += S.T1[i];
+    __syncthreads();
+    return;
+  }
   for (int i = threadIdx.x; i < mf * mf * mf; i += CV_NT) {  // [xf][yf][zf]
     const int zf = i % mf, t = i / mf, yf = t % mf, xf = t / mf;
     Xf[i] += cv_tv<K>(P, 1, Nc, xf, S.T1 + yf * mf + zf, mf * mf);
@@ -205,7 +228,7 @@ __device__ void cv_prolong(const CVShared& S, const double* P, int l) {
 template <int K>
 __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int blk, bool zero_start,
                           double lamp, double taup, bool& bad) {
-  const CVLevel<K> L(l);
+  const CVLevel<K> L(l, S.dim);
   const int m = L.m, n = L.n;
   const int ncoef = 1 + 2 * (a.deg - 1);
   const double* cf = a.coef + ((long long)l * a.nblk + blk) * ncoef;
@@ -264,25 +287,26 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   // per-block global scratch -- L2-resident, so the top level may be larger than the smem budget
   // would allow for all nine of its vectors
   CVShared S;
-  const int nmax = CVLevel<K>(lc).n;
+  S.dim = a.dim;
+  const int nmax = CVLevel<K>(lc, a.dim).n;
   double* p = sm;
   S.T0 = p; p += nmax;
   S.T1 = p; p += nmax;
   S.T2 = p; p += nmax;
   S.T3 = p; p += nmax;
   for (int l = 0; l < lc; ++l) {
-    const CVLevel<K> L(l);
+    const CVLevel<K> L(l, a.dim);
     S.X[l] = p; p += L.n;
     S.B[l] = p; p += L.n;
   }
   for (int l = 1; l <= lc; ++l) {
     S.DI[l] = p;
-    p += CVLevel<K>(l).n;
+    p += CVLevel<K>(l, a.dim).n;
   }
   {
     int* ip = reinterpret_cast<int*>(p);
     for (int l = 0; l <= lc; ++l) {
-      const CVLevel<K> L(l);
+      const CVLevel<K> L(l, a.dim);
       for (int i = threadIdx.x; i < L.n; i += CV_NT) {
         const int z = i % L.m, t = i / L.m, y = t % L.m, x = t / L.m;
         ip[i] = x | (y << 10) | (z << 20);
@@ -304,11 +328,11 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   __syncthreads();
   const double lam = a.lam[blk];
   for (int l = 1; l <= lc; ++l) {
-    const CVLevel<K> L(l);
+    const CVLevel<K> L(l, a.dim);
     const double lamp = lam * a.hd[l], taup = a.tau * a.hk[l];
     for (int i = threadIdx.x; i < L.n; i += CV_NT) {
       const int z = i % L.m, t = i / L.m, y = t % L.m, x = t / L.m;
-      S.DI[l][i] = cv_dinv<K>(x, y, z, L.m, lamp, taup);
+      S.DI[l][i] = cv_dinv<K>(x, y, z, L.m, L.mx, lamp, taup);
     }
   }
   __syncthreads();
@@ -320,14 +344,14 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
     const double lamp = lam * a.hd[l], taup = a.tau * a.hk[l];
     cv_smooth<K>(S, a, l, blk, true, lamp, taup, bad[l]);
     cv_apply<K>(S, l, S.X[l], S.W, lamp, taup);
-    const int n = CVLevel<K>(l).n;
+    const int n = CVLevel<K>(l, a.dim).n;
     for (int i = threadIdx.x; i < n; i += CV_NT) S.R[i] = S.B[l][i] - S.W[i];
     __syncthreads();
     cv_restrict<K>(S, a.P, l);
   }
   // coarse: x_0 = Cinv b_0 (dense inverse of the assembled constrained operator)
   {
-    const int n0 = CVLevel<K>(0).n;
+    const int n0 = CVLevel<K>(0, a.dim).n;
     const double* C = a.cinv + (long long)blk * n0 * n0;
     for (int i = threadIdx.x; i < n0; i += CV_NT) {
       double acc = 0.0;
@@ -351,28 +375,22 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
 
 }  // namespace
 
-long long spk_coarse_vcycle_smem(int K, int lc) {
+long long spk_coarse_vcycle_smem(int K, int lc, int dim) {
+  auto nodes = [&](int l) {
+    const long long m = ((long long)K << l) + 1;
+    return dim == 3 ? m * m * m : m * m;
+  };
   long long tot = 0;
-  for (int l = 0; l < lc; ++l) {
-    const long long m = ((long long)K << l) + 1;
-    tot += 2 * m * m * m;
-  }
-  for (int l = 1; l <= lc; ++l) {  // Jacobi tables
-    const long long m = ((long long)K << l) + 1;
-    tot += m * m * m;
-  }
+  for (int l = 0; l < lc; ++l) tot += 2 * nodes(l);
+  for (int l = 1; l <= lc; ++l) tot += nodes(l);  // Jacobi tables
   long long ints = 0;
-  for (int l = 0; l <= lc; ++l) {  // coordinate tables
-    const long long m = ((long long)K << l) + 1;
-    ints += m * m * m;
-  }
+  for (int l = 0; l <= lc; ++l) ints += nodes(l);  // coordinate tables
   tot += (ints + 1) / 2;
-  const long long m = ((long long)K << lc) + 1;
-  return (tot + 4 * m * m * m) * (long long)sizeof(double);
+  return (tot + 4 * nodes(lc)) * (long long)sizeof(double);
 }
 
 cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t s) {
-  const long long bytes = spk_coarse_vcycle_smem(K, a.lc);
+  const long long bytes = spk_coarse_vcycle_smem(K, a.lc, a.dim);
   if (a.lc < 1 || a.lc > SPK_CV_LMAX || bytes > SPK_CV_SMEM_MAX) return cudaErrorInvalidValue;
   switch (K) {
 #define SPK_CV(KK)                                                                                   \

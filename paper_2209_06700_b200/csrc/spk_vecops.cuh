@@ -108,10 +108,10 @@ cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_
 #define SPK_CV_LMAX 4
 #define SPK_CV_SMEM_MAX (200 * 1024)
 struct SpkCoarseArgs {
-  int lc, nblk, deg;
+  int lc, nblk, deg, dim;  // dim: 2 or 3 (2D: degenerate x axis)
   double tau;
   double lam[SPK_BMAX];                            // block shifts (unscaled)
-  double hd[SPK_CV_LMAX + 1], hk[SPK_CV_LMAX + 1];  // h^3, h per level
+  double hd[SPK_CV_LMAX + 1], hk[SPK_CV_LMAX + 1];  // h^dim, h^(dim-2) per level
   double P[(2 * SPK_KMAX + 1) * (SPK_KMAX + 1)];   // 1D prolongation table
   const double* coef;  // [lc+1][nblk][1 + 2(deg-1)]: theta, (c1, c2) per inner step
   const double* cinv;  // (nblk, n0, n0) row-major inverse of the constrained coarse operator
@@ -121,7 +121,7 @@ struct SpkCoarseArgs {
   double* scratch;     // (nblk, 3, n_lc): r, d, w of every level (global, L2-resident)
   long long sb, sx;
 };
-long long spk_coarse_vcycle_smem(int K, int lc);
+long long spk_coarse_vcycle_smem(int K, int lc, int dim);
 cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t s);
 
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);

@@ -27,6 +27,13 @@
 #ifndef SPK_MINB_ALL
 #define SPK_MINB_ALL 1
 #endif
+// Split plane barrier: each thread arrives on an mbarrier once its Z(t) / Y(t-1) results (and its
+// cp.async of plane t+1) are in shared memory, THEN runs X(t-2), and waits for the others' arrivals
+// only at the start of the next interval, so the X-phase of the warps with the most Z/Y work overlaps
+// the next interval of the others (MA/C triple-buffered for it).
+#ifndef SPK_SPLIT_BAR
+#define SPK_SPLIT_BAR 1
+#endif
 
 namespace {
 
@@ -52,6 +59,7 @@ template <int K, int Q> struct Geo {
   static constexpr bool PIPE3 = true;
   static constexpr int NT = (Q >= 2 && TY * TZ > 256) ? 512 : 256;
   static constexpr int NBUF = PIPE3 ? 2 : 1;
+  static constexpr int MCBUF = SPK_SPLIT_BAR ? 3 : NBUF;  // (MA, C) plane buffers
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
   static constexpr int TZp = TZ | 1;
@@ -65,7 +73,7 @@ template <int K, int Q> struct Geo {
   // Jacobi table: one entry per (x,y,z) node class ((K+1)^3) and block (block mode) / (A, B) (pair)
   static constexpr int DT_STRIDE = (Q > 2 ? Q : 2);
   static constexpr int DT_SZ = (K + 1) * (K + 1) * (K + 1) * DT_STRIDE;
-  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * NBUF * MC_SZ + DT_SZ + 2;  // + 2 mbarriers
+  static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * MCBUF * MC_SZ + DT_SZ + 4;  // + mbarriers
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
 #ifdef SPK_ZS
@@ -156,6 +164,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -457,8 +468,9 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   double* Us = smem;                    // [2][Q][NYin][NZp]
   double* ABs = Us + 2 * G::U_SZ;       // [2][Q][NYin][TZp] of (A, B) pairs (16-byte accesses)
   double* MCs = ABs + 2 * G::NBUF * G::AB_SZ;  // [NBUF][Q][TY][TZp] of (MA, C) pairs
-  double* dtab = MCs + 2 * G::NBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
+  double* dtab = MCs + 2 * G::MCBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
   unsigned long long* ubar = reinterpret_cast<unsigned long long*>(dtab + G::DT_SZ);  // plane-buffer mbarriers
+  unsigned long long* ibar = ubar + 2;  // split plane barrier (SPK_SPLIT_BAR)
   // interior tiles load their planes with bulk-async copies (one per row, issued by warp 0) that
   // complete on ubar[slot]; every other tile keeps the per-node cp.async path with zero-fill
   constexpr bool BULK = FULL && SPK_BULK_LOAD;
@@ -722,8 +734,8 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   };
 
   // ---------------- Y-phase: MA = My A, C = Ky A + My B ----------------
-  auto yphase = [&](auto PB) {
-    const int ab = parity_of(PB), mc = ab;
+  auto yphase = [&](auto PB, int mcbuf = -1) {
+    const int ab = parity_of(PB), mc = mcbuf >= 0 ? mcbuf : ab;
     const double2* AB = reinterpret_cast<const double2*>(ABs + ab * 2 * G::AB_SZ);
     double2* MC = reinterpret_cast<double2*>(MCs + mc * 2 * G::MC_SZ);
     if (ydeg) {
@@ -912,6 +924,17 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // Three-stage software pipeline, ONE barrier per plane: interval t runs Z(t), Y(t-1), X(t-2) on
   // disjoint double buffers (U/AB/MC indexed by plane parity) while U(t+1) is in flight. The loop is
   // unrolled by two so every buffer address is a compile-time offset.
+  // split barrier: interval t waits for interval t-1's arrivals; MA/C plane t lives in buffer t % 3
+  auto interval_split = [&](auto P, int t) {
+    constexpr int p = decltype(P)::value;  // == t & 1
+    if (t >= 1) mbar_wait(ibar, static_cast<unsigned>(t - 1) & 1u);
+    if (t + 1 < nplanes) load_plane(xs + t + 1, IC<1 - p>{});
+    if (t < nplanes) zphase(IC<p>{}, xs + t);
+    if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{}, (t - 1) % 3);
+    cp_async_wait_all();  // this thread's part of plane t+1 has landed
+    mbar_arrive(ibar);
+    if (t >= 2) xphase(xs + t - 2, (t - 2) % 3);
+  };
   auto interval = [&](auto P, int t) {
     constexpr int p = decltype(P)::value;  // == t & 1
     if constexpr (BULK) {
@@ -939,7 +962,19 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // instantiation except the stage-coupled k=2, Q=4 mix (C4's GMRES operator), whose doubled code
   // is slower (623 vs 575 us)
   constexpr bool UNROLL2 = BLOCK || !(K == 2 && Q == 4);
-  if constexpr (UNROLL2) {
+  if constexpr (SPK_SPLIT_BAR && !BULK) {
+    if (tid == 0) {
+      mbar_init(ibar, NT);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cp_async_wait_all();
+    __syncthreads();  // plane 0 in shared memory, barrier initialised
+    for (int t = 0; t < nplanes + 2; t += 2) {
+      interval_split(IC<0>{}, t);
+      if (t + 1 < nplanes + 2) interval_split(IC<1>{}, t + 1);
+    }
+    __syncthreads();
+  } else if constexpr (UNROLL2) {
     for (int t = 0; t < nplanes + 2; t += 2) {
       interval(IC<0>{}, t);
       if (t + 1 < nplanes + 2) interval(IC<1>{}, t + 1);

@@ -22,6 +22,8 @@ from . import _lib
 from ._device import is_host, like_input, ptr, require_cuda, stream_ptr, to_device
 from .errors import ConfigurationError, DimensionMismatchError
 
+_DEFERRED_CTX = []  # contexts collected during a CUDA graph capture, destroyed at the next chance
+
 MAX_DEGREE = 4
 
 
@@ -144,7 +146,12 @@ class GridHierarchy:
 
     def __del__(self):
         try:
+            if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+                _DEFERRED_CTX.append(self._ctx)  # no cudaFree inside a graph capture
+                return
             _lib.load().spk_ctx_destroy(self._ctx)
+            while _DEFERRED_CTX:
+                _lib.load().spk_ctx_destroy(_DEFERRED_CTX.pop())
         except Exception:
             pass
 

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import ptr, stream_ptr
+from ._device import capture_graph, ptr, stream_ptr
 from .errors import ConfigurationError, StepFailureError
 from .fem import SeparableSolution
 from .krylov import GraphedIterations, gmres
@@ -126,7 +126,7 @@ class StageSystem:
             self._precond_body(self._g_in, self._g_out)  # warm-up: configures kernels, allocates
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with capture_graph(g):
                 self._precond_body(self._g_in, self._g_out)
             self._graph = g
         self._g_in.copy_(r.reshape(self.Q, self.n))

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import ptr, require_cuda, stream_ptr
+from ._device import capture_graph, ptr, require_cuda, stream_ptr
 from .errors import NumericalFailureError
 
 BREAKDOWN_TOL = 1e-30
@@ -209,7 +209,7 @@ class GraphedIterations:
         g = self.graphs.get(j)
         if g is None:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with capture_graph(g):
                 self.outs[j] = self._body(j)
             self.graphs[j] = g
         g.replay()

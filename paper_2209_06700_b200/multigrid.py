@@ -250,7 +250,7 @@ class _DeviceVCycle:
             self._bufs[level] = _Level(self.nrows, h.levels[level].n_dofs, h.device, level < h.max_level)
         self._flags = torch.zeros(h.max_level + 1, dtype=torch.int32, device=h.device)
         self._cv_level = -1
-        if (self._fuse_coarse and not self.pair and h.dim == 3 and self.min_level == 0
+        if (self._fuse_coarse and not self.pair and h.dim >= 2 and self.min_level == 0
                 and self.config.coarse_solver == "direct" and self.nrows <= 16):
             lc = min(int(_lib.load().spk_coarse_vcycle_level(h.ctx)), h.max_level)
             if lc >= 1:
