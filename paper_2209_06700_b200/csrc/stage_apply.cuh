@@ -59,7 +59,6 @@ template <int K, int Q> struct Geo {
   static constexpr bool PIPE3 = true;
   static constexpr int NT = (Q >= 2 && TY * TZ > 256) ? 512 : 256;
   static constexpr int NBUF = PIPE3 ? 2 : 1;
-  static constexpr int MCBUF = SPK_SPLIT_BAR ? 3 : NBUF;  // (MA, C) plane buffers
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
   static constexpr int TZp = TZ | 1;
@@ -73,6 +72,12 @@ template <int K, int Q> struct Geo {
   // Jacobi table: one entry per (x,y,z) node class ((K+1)^3) and block (block mode) / (A, B) (pair)
   static constexpr int DT_STRIDE = (Q > 2 ? Q : 2);
   static constexpr int DT_SZ = (K + 1) * (K + 1) * (K + 1) * DT_STRIDE;
+  // split barrier (SPK_SPLIT_BAR) where it was measured to pay (profiles/r02_k1_ab.txt): k = 4
+  // (C2 426 -> 408 us); at k = 2 / 3 it lost 2-32 % (at k = 2, Q = 4 the third (MA, C) buffer also
+  // pushes the CTA past two per SM)
+  static constexpr int SMEM_SPLIT = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * 3 * MC_SZ + DT_SZ + 4;
+  static constexpr bool SPLIT = SPK_SPLIT_BAR && K == 4 && NT == 256 && SMEM_SPLIT * 8 <= 112 * 1024;
+  static constexpr int MCBUF = SPLIT ? 3 : NBUF;  // (MA, C) plane buffers
   static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * MCBUF * MC_SZ + DT_SZ + 4;  // + mbarriers
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
   // Z items: (q, yy, element segment), ZS elements per segment
@@ -962,7 +967,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // instantiation except the stage-coupled k=2, Q=4 mix (C4's GMRES operator), whose doubled code
   // is slower (623 vs 575 us)
   constexpr bool UNROLL2 = BLOCK || !(K == 2 && Q == 4);
-  if constexpr (SPK_SPLIT_BAR && !BULK) {
+  if constexpr (G::SPLIT && !BULK) {
     if (tid == 0) {
       mbar_init(ibar, NT);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");

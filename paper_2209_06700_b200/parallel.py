@@ -46,12 +46,11 @@ class SlabLayout:
         return slice(p0 * self.plane, p1 * self.plane)
 
 
-def exchange_halo(buf, layout, group=None):
-    """Fill the halo planes of buf (Q, local_numel) from the neighbouring ranks (grouped P2P).
-
-    Right neighbour receives my last k owned planes into its left halo; left neighbour receives my
-    first owned plane into its right halo plane.
-    """
+def exchange_halo_start(buf, layout, group=None):
+    """Post the halo exchange of buf (Q, local_numel) (grouped P2P; on NCCL the transfers run on
+    the communicator's stream): right neighbour receives my last k owned planes into its left halo,
+    left neighbour receives my first owned plane into its right halo plane. Returns the pending
+    state for exchange_halo_finish."""
     k, E, r, W = layout.k, layout.E, layout.rank, layout.world
     ops = []
     recv_bufs = []
@@ -75,16 +74,30 @@ def exchange_halo(buf, layout, group=None):
             tmp = torch.empty_like(lv, device="cpu" if host else lv.device)
             recv_bufs.append((lv, tmp))
             ops.append(dist.P2POp(dist.irecv, tmp, r - 1, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    return reqs, recv_bufs, len(ops)
+
+
+def exchange_halo_finish(pending):
+    """Wait for the posted exchange (stream-ordered on NCCL) and write the received halo planes."""
+    reqs, recv_bufs, nops = pending
+    for req in reqs:
+        req.wait()
     for dst, tmp in recv_bufs:
         dst.copy_(tmp)
-    return len(ops)
+    return nops
+
+
+def exchange_halo(buf, layout, group=None):
+    """Blocking form: fill the halo planes of buf (Q, local_numel) from the neighbouring ranks."""
+    return exchange_halo_finish(exchange_halo_start(buf, layout, group))
 
 
 class SlabOperator:
-    """K1 on an x-slab of a world*E x E x E element mesh: halo exchange + one windowed launch."""
+    """K1 on an x-slab of a world*E x E x E element mesh. An apply posts the halo exchange, runs K1
+    on the interior elements (they read owned planes only) while the planes are in flight, then the
+    two edge elements once the halos have landed: the exchange overlaps the bulk of the operator.
+    Every node is produced with the same arithmetic as one launch over the whole slab."""
 
     def __init__(self, hier, level, DM, DK, world, rank, group=None):
         if hier.dim != 3:
@@ -98,7 +111,8 @@ class SlabOperator:
         self.plane = lvl.n_per_axis ** 2
         self.layout = SlabLayout(self.k, self.E, self.plane, world, rank)
         self.world, self.rank, self.group = world, rank, group
-        self.launches_per_apply = 1
+        self.overlap = self.E >= 4
+        self.launches_per_apply = 3 if self.overlap else 1
 
     def alloc(self):
         n = self.layout.local_numel
@@ -106,21 +120,36 @@ class SlabOperator:
                 torch.zeros((self.Q, n), dtype=torch.float64, device=self.hier.device))
 
     def apply(self, u, v):
-        exchange_halo(u, self.layout, self.group)
-        return self.launch(u, v)
+        if not self.overlap:
+            exchange_halo(u, self.layout, self.group)
+            return self.launch(u, v)
+        pending = exchange_halo_start(u, self.layout, self.group)
+        eb, ee = self._range()
+        self.launch(u, v, eb + 1, ee - 1)   # interior: planes K eb .. K (ee - 1), all owned
+        exchange_halo_finish(pending)
+        self.launch(u, v, eb, eb + 1)       # first owned element: reads the left halo element
+        self.launch(u, v, ee - 1, ee)       # last one: reads the right halo plane
+        return v
 
-    def launch(self, u, v):
-        """The windowed K1 launch alone (halos already in place)."""
+    def _range(self):
+        return (0, self.E) if self.rank == 0 else (1, self.E + 1)
+
+    def launch(self, u, v, eb=None, ee=None):
+        """A windowed K1 launch over local elements [eb, ee) (default: the whole slab; halos
+        already in place)."""
         lay = self.layout
         n = lay.local_numel
         if self.rank == 0:
             base_u = u[:, lay.plane_slice(self.k, lay.nplanes)]
             base_v = v[:, lay.plane_slice(self.k, lay.nplanes)]
-            x_elems, eb, ee = self.E, 0, self.E
+            x_elems = self.E
         else:
             base_u, base_v = u, v
-            x_elems, eb, ee = self.E + 1, 1, self.E + 1
-        store_last = 1 if self.rank == self.world - 1 else 0
+            x_elems = self.E + 1
+        e0, e1 = self._range()
+        eb = e0 if eb is None else eb
+        ee = e1 if ee is None else ee
+        store_last = 1 if (self.rank == self.world - 1 and ee == e1) else 0
         _lib.call("spk_stage_apply_slab", self.hier.ctx, self.level, self.Q,
                   self.DM.ctypes.data_as(_lib.P_dbl), self.DK.ctypes.data_as(_lib.P_dbl),
                   ptr(base_u), n, ptr(base_v), n, x_elems, eb, ee, store_last,

@@ -486,13 +486,28 @@ class GPUStageBackend:
         return self.solver.apply_device(w.contiguous(), check=False)
 
     def stage_rhs(self, t_n, u_n, ctau):
+        """w_j = F(t_n + c_j tau) - K (mask u_n) for the own stages, one spk_rhs launch (identity mix:
+        masking w here does not change mask * (A^-1 w), which the stepper forms next)."""
         um = torch.where(self.maskt, u_n, torch.zeros_like(u_n)).reshape(1, -1)
-        ku = self.h.apply_block(self.L, 0.0, 1.0, um)[0]
-        fhat = torch.empty_like(u_n)
+        self._exchange_rhs(um)
+        ku = self.h.apply_block(self.L, 0.0, 1.0, um)
+        return self._rhs(t_n, ctau, ku, u_n)
+
+    def _exchange_rhs(self, um):
+        pass
+
+    def _rhs(self, t_n, ctau, ku, u_n):
         from . import _lib
         from ._device import ptr, stream_ptr
-        _lib.call("spk_outer3", self.h.ctx, self.L, ptr(self.g1), ptr(fhat), stream_ptr(self.h.device))
-        return torch.stack([self.source.F(t_n + ct) * fhat - ku for ct in ctau])
+        q = len(ctau)
+        out = torch.empty((q, u_n.numel()), dtype=torch.float64, device=u_n.device)
+        if q == 0:
+            return out
+        T = _lib.dbl_array([self.source.F(t_n + ct) for ct in ctau])
+        eye = np.ascontiguousarray(np.eye(q))
+        _lib.call("spk_rhs", self.h.ctx, self.L, q, ptr(self.g1), T, eye.ctypes.data_as(_lib.P_dbl), ptr(ku),
+                  ptr(out), stream_ptr(self.h.device))
+        return out
 
 
 class GPUSlabStageBackend(GPUStageBackend):
@@ -521,15 +536,8 @@ class GPUSlabStageBackend(GPUStageBackend):
         self.part.exchange(km, self.L)
         return (self.h.apply_block(self.L, 1.0, 0.0, km), self.h.apply_block(self.L, 0.0, 1.0, km))
 
-    def stage_rhs(self, t_n, u_n, ctau):
-        um = torch.where(self.maskt, u_n, torch.zeros_like(u_n)).reshape(1, -1)
+    def _exchange_rhs(self, um):
         self.part.exchange(um, self.L)
-        ku = self.h.apply_block(self.L, 0.0, 1.0, um)[0]
-        fhat = torch.empty_like(u_n)
-        from . import _lib
-        from ._device import ptr, stream_ptr
-        _lib.call("spk_outer3", self.h.ctx, self.L, ptr(self.g1), ptr(fhat), stream_ptr(self.h.device))
-        return torch.stack([self.source.F(t_n + ct) * fhat - ku for ct in ctau])
 
 
 class DirectComplexParallelStepper:
