@@ -11,6 +11,7 @@
 #define SPK_KMAX 4       // highest Q_k degree with a compiled kernel
 #define SPK_QMAX 4       // highest stage count of the fused stage-coupled kernel
 #define SPK_BMAX 16      // per-launch block-parameter slots (block mode)
+#define SPK_ZTAIL_MAX 160  // K1 Z-phase tail items (Q * segments * (rows - 16)) with a host order
 #define SPK_THREADS 256
 #define SPK_SMALL_WORK_HOST (1LL << 23)  // = SPK_SMALL_WORK (stage_apply.cuh): direct small-level kernel
 
@@ -74,6 +75,8 @@ struct SpkApplyArgs {
   double hd, hk;          // host only: h^dim and h^(dim-2) folded into the mix by the launcher
   int final_step;         // EPI_CHEB: last step -> write x + d_new only (fused x + d), NaN flag
   int* nan_flag;
+  // K1 Z-phase: order of the items past the first 16 rows (host-computed, conflict-free STS.128)
+  unsigned char ztail[SPK_ZTAIL_MAX];
 };
 
 // ---- programmatic dependent launch (PDL) ------------------------------------------------------

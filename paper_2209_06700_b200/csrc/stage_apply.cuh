@@ -21,6 +21,7 @@
 // HBM traffic per apply: read u once (+ L2-resident halo), write v once = 16 B per stage-DoF.
 #pragma once
 #include <algorithm>
+#include <cstring>
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
 
@@ -177,12 +178,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// (with a suspend-time hint the waiting thread sleeps in the barrier instead of re-polling: the
+// polling loop was ~11 % of K1's issued instructions, profiles/r02_stage_apply_ncu_summary.txt)
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "SPK_MBAR_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra SPK_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase)
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra SPK_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase), "r"(0x989680u)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -654,7 +657,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
         qs = it / R;
         yy = it - qs * R;
       } else {
-        const int idx = it - QS * R;
+        // rows past the first 16: the launcher's order (ztail_order), in which every 8 consecutive
+        // lanes write 8 distinct 16-byte slots of the (A, B) buffer
+        constexpr int T = QS * (NYin - R);
+        const int idx = T <= SPK_ZTAIL_MAX ? static_cast<int>(a.ztail[it - QS * R]) : it - QS * R;
         yy = R + idx / QS;
         qs = idx - (yy - R) * QS;
       }
@@ -1197,9 +1203,50 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
   }
 }
 
-template <int K, int Q, bool BLOCK, int EPI>
-cudaError_t launch_one(const SpkApplyArgs& a, cudaStream_t s, int* nctas_out) {
+// Host: order of K1's Z-phase tail items (rows >= 16 of every (stage, segment)) such that each group
+// of 8 consecutive items writes 8 distinct 16-byte slots (slot = (row * TZp + zl) mod 8 in double2
+// units) -- greedy, once per geometry. Passed in the kernel parameters (computing it per thread at
+// CTA setup cost more than it saved: profiles/r02_k1_ab.txt).
+template <int K, int Q>
+const unsigned char* ztail_order() {
   using G = Geo<K, Q>;
+  constexpr int R = G::NYin < 16 ? G::NYin : 16;
+  constexpr int QS = Q * G::ZSEG;
+  constexpr int T = QS * (G::NYin - R);
+  static unsigned char tab[SPK_ZTAIL_MAX] = {};
+  static bool done = false;
+  if (done || T <= 0 || T > SPK_ZTAIL_MAX) return tab;
+  bool used[SPK_ZTAIL_MAX] = {};
+  int pos = 0;
+  while (pos < T) {
+    unsigned slots = 0u;
+    int got = 0;
+    for (int c = 0; c < T && got < 8; ++c) {
+      if (used[c]) continue;
+      const int yy = R + c / QS, qs = c % QS, q = qs / G::ZSEG, seg = qs % G::ZSEG;
+      const int sl = ((q * G::NYin + yy) * G::TZp + K * seg * G::ZS) & 7;
+      if ((slots >> sl) & 1u) continue;
+      slots |= 1u << sl;
+      used[c] = true;
+      tab[pos++] = static_cast<unsigned char>(c);
+      ++got;
+    }
+    for (int c = 0; c < T && got < 8; ++c)
+      if (!used[c]) {
+        used[c] = true;
+        tab[pos++] = static_cast<unsigned char>(c);
+        ++got;
+      }
+  }
+  done = true;
+  return tab;
+}
+
+template <int K, int Q, bool BLOCK, int EPI>
+cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out) {
+  using G = Geo<K, Q>;
+  SpkApplyArgs a = a_in;
+  std::memcpy(a.ztail, ztail_order<K, Q>(), SPK_ZTAIL_MAX);
   constexpr long long W3 = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);
   if constexpr (BLOCK) {
     // small whole-mesh levels: direct gather kernel (no plane pipeline)
