@@ -1039,6 +1039,8 @@ int spk_coarse_vcycle(spk_ctx* c, int lc, int nblk, const double* lams, double t
   SpkCoarseArgs a;
   std::memset(&a, 0, sizeof(a));
   a.lc = lc; a.nblk = nblk; a.deg = deg; a.tau = tau; a.dim = c->dim;
+  a.top_in_smem = (spk_coarse_vcycle_smem(c->K, lc, c->dim) + spk_coarse_vcycle_top_bytes(c->K, lc, c->dim) <=
+                   SPK_CV_SMEM_MAX && std::getenv("SPK_CV_TOP_GLOBAL") == nullptr) ? 1 : 0;
   for (int i = 0; i < nblk; ++i) a.lam[i] = lams[i];
   for (int l = 0; l <= lc; ++l) {  // M = h^d M_hat, K = h^(d-2) K_hat on the reference tables
     a.hd[l] = std::pow(c->h[l], c->dim);

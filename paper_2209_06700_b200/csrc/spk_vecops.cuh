@@ -109,6 +109,7 @@ cudaError_t spk_launch_cheb_rows(int K, int op, const SpkRowArgs& a, cudaStream_
 #define SPK_CV_SMEM_MAX (200 * 1024)
 struct SpkCoarseArgs {
   int lc, nblk, deg, dim;  // dim: 2 or 3 (2D: degenerate x axis)
+  int top_in_smem;         // level lc's x, b, r, d, w in shared memory (else global / L2)
   double tau;
   double lam[SPK_BMAX];                            // block shifts (unscaled)
   double hd[SPK_CV_LMAX + 1], hk[SPK_CV_LMAX + 1];  // h^dim, h^(dim-2) per level
@@ -122,6 +123,7 @@ struct SpkCoarseArgs {
   long long sb, sx;
 };
 long long spk_coarse_vcycle_smem(int K, int lc, int dim);
+long long spk_coarse_vcycle_top_bytes(int K, int lc, int dim);
 cudaError_t spk_launch_coarse_vcycle(int K, const SpkCoarseArgs& a, cudaStream_t s);
 
 cudaError_t spk_launch_transfer(int K, const SpkTransferArgs& a, cudaStream_t s);

@@ -35,6 +35,10 @@
 #ifndef SPK_SPLIT_BAR
 #define SPK_SPLIT_BAR 1
 #endif
+// bulk-async (TMA engine) row copies for interior tiles: measured and rejected, see load_plane_bulk
+#ifndef SPK_BULK_LOAD
+#define SPK_BULK_LOAD 0
+#endif
 
 namespace {
 
@@ -45,7 +49,10 @@ template <int K> struct Tile;
 template <> struct Tile<1> { static constexpr int TYE = 16, TZE = 16; };
 template <> struct Tile<2> { static constexpr int TYE = 8, TZE = 8; };
 template <> struct Tile<3> { static constexpr int TYE = 5, TZE = 5; };
-template <> struct Tile<4> { static constexpr int TYE = 4, TZE = 4; };
+#ifndef SPK_K4_TZE
+#define SPK_K4_TZE 4
+#endif
+template <> struct Tile<4> { static constexpr int TYE = 4, TZE = SPK_K4_TZE; };
 
 #ifndef SPK_Q1_TILE
 #define SPK_Q1_TILE 1
@@ -58,7 +65,7 @@ template <int K, int Q> struct Geo {
   static constexpr int TY = K * TYE, TZ = K * TZE;
   // 1 barrier per plane: Z, Y, X run on three plane buffers (see the pipeline below)
   static constexpr bool PIPE3 = true;
-  static constexpr int NT = (Q >= 2 && TY * TZ > 256) ? 512 : 256;
+  static constexpr int NT = (Q >= 2 && TY * TZ > 256) ? 512 : (TY * TZ < 256 && TY * TZ > 128 ? (TY * TZ + 31) / 32 * 32 : 256);
   static constexpr int NBUF = PIPE3 ? 2 : 1;
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
@@ -66,7 +73,7 @@ template <int K, int Q> struct Geo {
   // bulk-copy layout (interior tiles, SPK_BULK_LOAD): 16-byte aligned rows of NZb doubles, each holding
   // its NZin values at a per-row offset of 0 or 1 (the global row start rounded down to 16 bytes)
   static constexpr int NZb = (NZin + 2) & ~1;
-  static constexpr int U_SZ = Q * NYin * (NZp > NZb ? NZp : NZb);  // one plane buffer
+  static constexpr int U_SZ = Q * NYin * ((SPK_BULK_LOAD && NZb > NZp) ? NZb : NZp);  // one plane buffer
   static constexpr int BROWS = Q * NYin;                           // bulk copies per plane
   static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
   static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
@@ -77,7 +84,8 @@ template <int K, int Q> struct Geo {
   // (C2 426 -> 408 us); at k = 2 / 3 it lost 2-32 % (at k = 2, Q = 4 the third (MA, C) buffer also
   // pushes the CTA past two per SM)
   static constexpr int SMEM_SPLIT = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * 3 * MC_SZ + DT_SZ + 4;
-  static constexpr bool SPLIT = SPK_SPLIT_BAR && K == 4 && NT == 256 && SMEM_SPLIT * 8 <= 112 * 1024;
+  static constexpr bool SPLIT = SPK_SPLIT_BAR && K == 4 && NT <= 256 &&
+                                (NT == 256 ? SMEM_SPLIT * 8 <= 112 * 1024 : SMEM_SPLIT * 8 <= 74 * 1024);
   static constexpr int MCBUF = SPLIT ? 3 : NBUF;  // (MA, C) plane buffers
   static constexpr int SMEM_DOUBLES = 2 * U_SZ + 2 * NBUF * AB_SZ + 2 * MCBUF * MC_SZ + DT_SZ + 4;  // + mbarriers
   static constexpr int PPT = (TY * TZ + NT - 1) / NT;
@@ -103,7 +111,9 @@ template <int K, int Q> struct Geo {
   static constexpr int LITEMS = Q * NYin * NZin;
   static constexpr int LIT = (LITEMS + NT - 1) / NT;
   static_assert(LIT <= 32, "load items are flagged in one 32-bit mask");
-  static constexpr int MINB = (NT == 256 && SMEM_DOUBLES * 8 <= 112 * 1024) ? 2 : 1;
+  static constexpr int MINB = (NT <= 192 && SMEM_DOUBLES * 8 <= 74 * 1024)   ? 3
+                              : (NT <= 256 && SMEM_DOUBLES * 8 <= 112 * 1024) ? 2
+                                                                              : 1;
 };
 
 // Distinct entries of a symmetric, centro-symmetric (K+1)x(K+1) element table:
@@ -204,9 +214,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // engine, and the 16-byte aligned rows cost the Z-phase its odd-pitch conflict-free reads. The n_ax =
 // k 2^l + 1 layout (odd row stride, 2056 bytes at C2) rules out 2D/3D tensor maps (TMA needs
 // 16-byte multiple strides), so a plane cannot be one TMA box. Kept behind -DSPK_BULK_LOAD=1.
-#ifndef SPK_BULK_LOAD
-#define SPK_BULK_LOAD 0
-#endif
+// (SPK_BULK_LOAD: defined at the top of this file)
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // assembled 1D reference diagonal at node i of an axis with E elements (E == 0: degenerate axis)
