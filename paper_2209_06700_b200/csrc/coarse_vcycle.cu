@@ -67,9 +67,11 @@ struct CVShared {
   const double* bk;
 };
 
-// v = A u (constrained: boundary entries of u read as 0, boundary rows = identity)
-template <int K>
-__device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, double lamp, double taup) {
+// (A u)_i handed to epi(i, value) in the operator's last sweep (constrained: boundary entries of u
+// read as 0, boundary rows = identity). The caller's per-node update rides on that sweep instead of
+// taking a pass and a barrier of its own; it may overwrite u (read in the first sweep only).
+template <int K, class Epi>
+__device__ void cv_apply(const CVShared& S, int l, const double* u, double lamp, double taup, Epi&& epi) {
   constexpr int W = 2 * K + 1;
   const CVLevel<K> L(l, S.dim);
   const int m = L.m, n = L.n, mm = m * m, mx = L.mx;
@@ -103,18 +105,20 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
       cc = fma(S.bk[c * W + d], S.T0[j], cc);
       cc = fma(S.bm[c * W + d], S.T1[j], cc);
     }
+    if (mx == 1) {  // 2D: v = p (degenerate x factors Mx = 1, Kx = 0); boundary rows identity
+      const int z = co[i] >> 20;
+      epi(i, cv_bnd(0, y, z, m, 1) ? u[i] : fma(lamp, ma, taup * cc));
+      continue;
+    }
     S.T2[i] = fma(lamp, ma, taup * cc);  // p
     S.T3[i] = taup * ma;                 // q
   }
   __syncthreads();
+  if (mx == 1) return;
   for (int i = threadIdx.x; i < n; i += CV_NT) {  // x: v = Mx p + Kx q ; boundary rows identity
     const int cw = co[i], x = cw & 1023, y = (cw >> 10) & 1023, z = cw >> 20;
     if (cv_bnd(x, y, z, m, mx)) {
-      v[i] = u[i];
-      continue;
-    }
-    if (mx == 1) {  // 2D: the degenerate x factors are Mx = 1, Kx = 0
-      v[i] = S.T2[i];
+      epi(i, u[i]);
       continue;
     }
     const int c = cv_cls<K>(x, m);
@@ -127,7 +131,7 @@ __device__ void cv_apply(const CVShared& S, int l, const double* u, double* v, d
       acc = fma(S.bm[c * W + d], S.T2[j], acc);
       acc = fma(S.bk[c * W + d], S.T3[j], acc);
     }
-    v[i] = acc;
+    epi(i, acc);
   }
   __syncthreads();
 }
@@ -235,14 +239,22 @@ __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int 
   const double theta = cf[0];
   double* X = S.X[l];
   const double* Bv = S.B[l];
-  if (!zero_start) cv_apply<K>(S, l, X, S.W, lamp, taup);
-  for (int i = threadIdx.x; i < n; i += CV_NT) {
-    const double r = zero_start ? Bv[i] : Bv[i] - S.W[i];
-    if (zero_start) X[i] = 0.0;
-    S.R[i] = r;
-    S.D[i] = (S.DI[l][i] * r) / theta;
+  const double* DI = S.DI[l];
+  if (!zero_start) {  // r = b - A x, d = Dinv r / theta (fused into the operator's last sweep)
+    cv_apply<K>(S, l, X, lamp, taup, [&](int i, double w) {
+      const double r = Bv[i] - w;
+      S.R[i] = r;
+      S.D[i] = (DI[i] * r) / theta;
+    });
+  } else {
+    for (int i = threadIdx.x; i < n; i += CV_NT) {
+      const double r = Bv[i];
+      X[i] = 0.0;
+      S.R[i] = r;
+      S.D[i] = (DI[i] * r) / theta;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (a.deg == 1) {
     for (int i = threadIdx.x; i < n; i += CV_NT) {
       const double xn = X[i] + S.D[i];
@@ -255,12 +267,12 @@ __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int 
   for (int k = 0; k < a.deg - 1; ++k) {
     const double c1 = cf[1 + 2 * k], c2 = cf[2 + 2 * k];
     const bool last = (k == a.deg - 2);
-    cv_apply<K>(S, l, S.D, S.W, lamp, taup);
-    for (int i = threadIdx.x; i < n; i += CV_NT) {
+    // w = A d with the step x += d; r -= w; d = c1 d + c2 Dinv r on each node in the same sweep
+    cv_apply<K>(S, l, S.D, lamp, taup, [&](int i, double w) {
       const double d = S.D[i];
       const double xn = X[i] + d;
-      const double r = S.R[i] - S.W[i];
-      const double dn = c1 * d + c2 * (S.DI[l][i] * r);
+      const double r = S.R[i] - w;
+      const double dn = c1 * d + c2 * (DI[i] * r);
       if (last) {
         const double xf = xn + dn;
         X[i] = xf;
@@ -270,8 +282,7 @@ __device__ void cv_smooth(const CVShared& S, const SpkCoarseArgs& a, int l, int 
         S.R[i] = r;
         S.D[i] = dn;
       }
-    }
-    __syncthreads();
+    });
   }
 }
 
@@ -364,10 +375,8 @@ __global__ void __launch_bounds__(CV_NT, 1) coarse_vcycle_kernel(const __grid_co
   for (int l = lc; l >= 1; --l) {
     const double lamp = lam * a.hd[l], taup = a.tau * a.hk[l];
     cv_smooth<K>(S, a, l, blk, true, lamp, taup, bad[l]);
-    cv_apply<K>(S, l, S.X[l], S.W, lamp, taup);
-    const int n = CVLevel<K>(l, a.dim).n;
-    for (int i = threadIdx.x; i < n; i += CV_NT) S.R[i] = S.B[l][i] - S.W[i];
-    __syncthreads();
+    const double* Bl = S.B[l];
+    cv_apply<K>(S, l, S.X[l], lamp, taup, [&](int i, double w) { S.R[i] = Bl[i] - w; });
     cv_restrict<K>(S, a.P, l);
   }
   // coarse: x_0 = Cinv b_0 (dense inverse of the assembled constrained operator)
