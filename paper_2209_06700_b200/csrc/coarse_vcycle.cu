@@ -19,7 +19,10 @@
 
 namespace {
 
-constexpr int CV_NT = 512;
+#ifndef SPK_CV_NT
+#define SPK_CV_NT 512
+#endif
+constexpr int CV_NT = SPK_CV_NT;
 
 template <int K>
 struct CVLevel {
