@@ -45,6 +45,12 @@ struct spk_ctx {
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
   long long split_cheb_min = 1LL << 18;
+  int per_cta2_epi = 1;   // epilogues (bit mask over SpkEpi) that take the two-per-CTA launch (SPK_PER_CTA2_EPI)
+  int vsplit_v = 0;       // virtual x-ranges per CTA of a single-block launch (SPK_VSPLIT_V: 4 or 2; 0: automatic)
+  // blocks swept together by one K1 CTA (SPK_PER_CTA_MAX; 0: two per CTA where SPK_PER_CTA2_* allow.
+  // Measured on C4: two per CTA wins the STORE launch alone, 531 -> 484 us, but not the step, 211 -> 220 ms)
+  int per_cta_max = 4;
+  long long per_cta2_min = 1LL << 16;  // ... two per CTA from this many nodes per block (SPK_PER_CTA2_MIN)
   int vsplit = 1;         // single-block K1 launches sweep 4 x-ranges per CTA (virtual x-split)
   // device scratch (lazily allocated on first device call)
   double* partial = nullptr;
@@ -255,7 +261,10 @@ int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, in
   // (not on levels the direct small-level kernel takes: stage_apply.cuh launch_one)
   if (nblk == 1 && c->vsplit && !small_level(c, level) && epi != EPI_CHEB && c->dim == 3 && g.Ex >= 8 && g.x0 == 0 &&
       a.ex_begin == 0 && (a.ex_end == 0 || a.ex_end == g.Ex)) {
-    const int V = (g.Ex % 4 == 0) ? 4 : 2;
+    // (degrees <= 3: two ranges per CTA at four CTAs per SM, stage_apply.cuh SPK_MINB4 -- measured C5
+    // 95.1 -> 89.0 ms / step, C5-gmg 77.7 -> 74.6)
+    const int vpref = c->vsplit_v > 0 ? c->vsplit_v : (c->K <= 3 ? 2 : 4);
+    const int V = (g.Ex % 4 == 0 && vpref != 2) ? 4 : 2;
     const int Ev = g.Ex / V;
     const long long vs = (long long)c->K * Ev * g.ny * g.nz;
     SpkApplyArgs b = a;
@@ -280,7 +289,12 @@ int apply_blocks_chunked(spk_ctx* c, int level, int nblk, const double* lams, in
   for (int b0 = 0; b0 < nblk;) {
     int nb = std::min(SPK_BMAX, nblk - b0);
     int per_cta = 1;
-    for (int q = 4; q >= 2; --q)
+    // low degrees, large levels, an even number of blocks: two blocks per CTA at four CTAs per SM
+    // (stage_apply.cuh SPK_MINB4) beat four per CTA at two
+    int qmax = c->per_cta_max;
+    if (qmax <= 0)
+      qmax = (c->K <= 3 && nb % 2 == 0 && a.g.n >= c->per_cta2_min && ((c->per_cta2_epi >> epi) & 1)) ? 2 : 4;
+    for (int q = qmax; q >= 2; --q)
       if (nb >= q) { per_cta = q; break; }
     nb = (nb / per_cta) * per_cta;
     a.blk_base = b0;
@@ -372,6 +386,10 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   spk_ctx* c = new spk_ctx();
   if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
   if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
+  if (const char* e = std::getenv("SPK_PER_CTA_MAX")) c->per_cta_max = std::max(0, std::min(4, std::atoi(e)));
+  if (const char* e = std::getenv("SPK_PER_CTA2_EPI")) c->per_cta2_epi = std::atoi(e);
+  if (const char* e = std::getenv("SPK_VSPLIT_V")) c->vsplit_v = std::atoi(e);
+  if (const char* e = std::getenv("SPK_PER_CTA2_MIN")) c->per_cta2_min = std::atoll(e);
   if (const char* e = std::getenv("SPK_FILL_WAVE")) c->fill_wave = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_TRANSFER")) c->fuse_transfer = std::atoi(e);
   if (const char* e = std::getenv("SPK_FUSE_RESTRICT_MAX")) c->fuse_restrict_max = std::atoll(e);

@@ -22,6 +22,7 @@
 #pragma once
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
 
@@ -111,7 +112,14 @@ template <int K, int Q> struct Geo {
   static constexpr int LITEMS = Q * NYin * NZin;
   static constexpr int LIT = (LITEMS + NT - 1) / NT;
   static_assert(LIT <= 32, "load items are flagged in one 32-bit mask");
-  static constexpr int MINB = (NT <= 192 && SMEM_DOUBLES * 8 <= 74 * 1024)   ? 3
+// Low degrees sweeping one or two blocks per CTA fit four CTAs per SM (64 registers, <= 55 KB): twice
+// the warps to hide the plane pipeline's latency (measured: C4 block STORE 531 -> 484 us with two
+// blocks per CTA). SPK_MINB4 = highest degree that gets the 4-CTA launch bound.
+#ifndef SPK_MINB4
+#define SPK_MINB4 3
+#endif
+  static constexpr int MINB = (SPK_MINB4 && K <= SPK_MINB4 && NT <= 256 && SMEM_DOUBLES * 8 <= 55 * 1024) ? 4
+                              : (NT <= 192 && SMEM_DOUBLES * 8 <= 74 * 1024)   ? 3
                               : (NT <= 256 && SMEM_DOUBLES * 8 <= 112 * 1024) ? 2
                                                                               : 1;
 };
@@ -1037,7 +1045,9 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
 #endif
 
 template <int K, int Q, bool BLOCK, int EPI>
-__global__ void __launch_bounds__(Geo<K, Q>::NT, SPK_MINB_ALL ? Geo<K, Q>::MINB : ((EPI == EPI_STORE || Q <= 2) ? Geo<K, Q>::MINB : 1))
+__global__ void __launch_bounds__(Geo<K, Q>::NT,
+                                  // (the fused Chebyshev epilogue spills at 64 registers: two CTAs)
+                                  (EPI == EPI_CHEB && Geo<K, Q>::MINB > 2) ? 2 : Geo<K, Q>::MINB)
     stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
   extern __shared__ __align__(16) double smem[];
   using G = Geo<K, Q>;
@@ -1211,6 +1221,25 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
   }
 }
 
+}  // namespace
+#include "stage_apply_ws.cuh"
+namespace {
+
+// K1w (stage_apply_ws.cuh) takes 3D launches on levels with at least SPK_WS_MIN nodes per axis
+// (SPK_WS=0: never)
+inline int spk_ws_min_nodes() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = std::getenv("SPK_WS");
+    if (e && e[0] == '0') v = -1;
+    else {
+      const char* m = std::getenv("SPK_WS_MIN");
+      v = m ? std::atoi(m) : 0;
+    }
+  }
+  return v;
+}
+
 // Host: order of K1's Z-phase tail items (rows >= 16 of every (stage, segment)) such that each group
 // of 8 consecutive items writes 8 distinct 16-byte slots (slot = (row * TZp + zl) mod 8 in double2
 // units) -- greedy, once per geometry. Passed in the kernel parameters (computing it per thread at
@@ -1280,6 +1309,13 @@ cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out)
         return spk_launch(small_apply_kernel<K, EPI, true>, grid, dim3(256), stage_bytes, s, a);
       }
       return spk_launch(small_apply_kernel<K, EPI, false>, grid, dim3(256), 0, s, a);
+    }
+  }
+  if constexpr (EPI != EPI_DINV) {
+    const int wsmin = spk_ws_min_nodes();
+    if (wsmin >= 0 && a.g.nz >= wsmin) {
+      SpkWsMaps maps;
+      if (ws_maps<K, Q>(a, BLOCK, &maps)) return launch_ws<K, Q, BLOCK, EPI>(a, maps, s, nctas_out);
     }
   }
   const size_t smem = sizeof(double) * G::SMEM_DOUBLES;

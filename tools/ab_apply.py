@@ -1,6 +1,6 @@
 """A/B of libspk variants on the K1 hot launches (one GPU session; CUDA events, median of 7).
 
-usage: python tools/ab_apply.py _variants/a.so _variants/b.so ...
+usage: python tools/ab_apply.py _variants/a.so _variants/b.so@SPK_WS=0 ...
 Each variant runs in its own process (SPK_LIB_PATH); outputs are compared against the first
 variant's (max relative difference), so a faster variant must also be parity-identical."""
 import json
@@ -50,7 +50,9 @@ def main():
     libs = sys.argv[1:]
     res = {}
     for lib in libs:
-        env = dict(os.environ, SPK_LIB_PATH=os.path.abspath(lib), SPK_LIB_LAX="1")
+        path, *sets = lib.split("@")   # variant = path[@ENV=VAL[@ENV=VAL...]]
+        env = dict(os.environ, SPK_LIB_PATH=os.path.abspath(path), SPK_LIB_LAX="1")
+        env.update(dict(kv.split("=", 1) for kv in sets))
         r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(CASES)], env=env, capture_output=True, text=True)
         line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT")]
         if not line:

@@ -14,7 +14,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def main():
     cfgs = sys.argv[1]
     for lib in sys.argv[2:]:
-        env = dict(os.environ, SPK_LIB_PATH=os.path.abspath(lib), SPK_LIB_LAX="1")
+        path, *sets = lib.split("@")   # variant = path[@ENV=VAL...]
+        env = dict(os.environ, SPK_LIB_PATH=os.path.abspath(path), SPK_LIB_LAX="1")
+        env.update(dict(kv.split("=", 1) for kv in sets))
         r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu", "--level", "4",
                             "--step-configs", cfgs], cwd=REPO, env=env, capture_output=True, text=True)
         line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
