@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
+#include <cuda.h>
 
 #ifndef SPK_MINB_ALL
 #define SPK_MINB_ALL 1
@@ -36,9 +37,9 @@
 #ifndef SPK_SPLIT_BAR
 #define SPK_SPLIT_BAR 1
 #endif
-// bulk-async (TMA engine) row copies for interior tiles: measured and rejected, see load_plane_bulk
-#ifndef SPK_BULK_LOAD
-#define SPK_BULK_LOAD 0
+// TMA plane loads for interior tiles (two 2D boxes per stage and plane, see load_plane_tma)
+#ifndef SPK_TMA_LOAD
+#define SPK_TMA_LOAD 1
 #endif
 
 namespace {
@@ -71,11 +72,20 @@ template <int K, int Q> struct Geo {
   static constexpr int NYin = TY + K + 1, NZin = TZ + K + 1;
   static constexpr int NZp = NZin | 1;   // odd pitch: lanes walking rows hit distinct banks
   static constexpr int TZp = TZ | 1;
-  // bulk-copy layout (interior tiles, SPK_BULK_LOAD): 16-byte aligned rows of NZb doubles, each holding
-  // its NZin values at a per-row offset of 0 or 1 (the global row start rounded down to 16 bytes)
-  static constexpr int NZb = (NZin + 2) & ~1;
-  static constexpr int U_SZ = Q * NYin * ((SPK_BULK_LOAD && NZb > NZp) ? NZb : NZp);  // one plane buffer
-  static constexpr int BROWS = Q * NYin;                           // bulk copies per plane
+  // TMA layout of a plane buffer (interior tiles): per stage an even-row and an odd-row box of BOXR
+  // rows x W doubles (see load_plane_tma). W: even (16-byte multiple), >= NZin + 1 (a row's values sit
+  // at offset 0 or 1 of its box row), W / 2 odd (16 consecutive rows hit 16 distinct banks)
+  static constexpr int wpitch() {
+    int w = (NZin + 2) & ~1;
+    while ((w / 2) % 2 == 0) w += 2;
+    return w;
+  }
+  static constexpr int W = wpitch();
+  static constexpr int BOXR = (NYin + 1) / 2;
+  static constexpr int REG = (BOXR * W + 15) / 16 * 16;  // one box, 128-byte multiple
+  static constexpr int U_SZT = Q * 2 * REG;
+  static constexpr unsigned TX_BYTES = 2u * Q * BOXR * W * 8u;
+  static constexpr int U_SZ = (SPK_TMA_LOAD && U_SZT > Q * NYin * NZp) ? U_SZT : Q * NYin * NZp;  // one plane buffer
   static constexpr int AB_SZ = Q * NYin * TZp;         // one of A / B
   static constexpr int MC_SZ = Q * TY * TZp;           // one of MA / C
   // Jacobi table: one entry per (x,y,z) node class ((K+1)^3) and block (block mode) / (A, B) (pair)
@@ -216,13 +226,32 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// Measured on B200 (tools/ab_apply.py, profiles/r02_k1_ab.txt) and REJECTED as the default: one
-// 176-byte bulk copy per row (63 per plane at C2, issued by warp 0) through the async copy engine
-// ran C2 at 711 us against 428 us for the per-node cp.async path -- the row copies serialise in the
-// engine, and the 16-byte aligned rows cost the Z-phase its odd-pitch conflict-free reads. The n_ax =
-// k 2^l + 1 layout (odd row stride, 2056 bytes at C2) rules out 2D/3D tensor maps (TMA needs
-// 16-byte multiple strides), so a plane cannot be one TMA box. Kept behind -DSPK_BULK_LOAD=1.
-// (SPK_BULK_LOAD: defined at the top of this file)
+// TMA plane loads and the reference layout. A level's row stride is n_ax * 8 bytes with n_ax = k 2^l + 1
+// odd -- not a legal tensor-map stride (16-byte multiples) -- but TWO rows are. The maps describe the
+// vector as  dim0 = flat element index from the 16-byte aligned base (stage, plane, row parity and z
+// offset go into the coordinate),  dim1 = row PAIR index inside a plane (stride 2 nz 8 bytes, exact
+// size: rows outside the plane are zero-filled), so a plane of a stage arrives as an even-row box
+// and an odd-row box of BOXR x W doubles. The box start must be 16-byte aligned (an odd start
+// coordinate traps: tools/ubench/tma_probe.cu), so it is the flat index of the tile's first loaded
+// node rounded down to even and a row's values sit at offset 0 or 1 of its box row; rows are an odd
+// number of doubles apart, so the two boxes get opposite offsets and 16 consecutive rows of the
+// (even-pitch) boxes hit 16 distinct banks in the Z sweep. One thread issues the 2 Q boxes of a
+// plane (SASS: UTMALDG.2D); they complete on the plane buffer's mbarrier.
+// (Round-2 history: one 176-byte cp.async.bulk per ROW, 63 per plane, ran C2 at 711 us and was
+// rejected: profiles/r02_k1_ab.txt.)
+struct SpkWsMaps {
+  CUtensorMap even, odd;
+  int bias;  // elements between the 16-byte aligned map base and args.u (0 or 1); < 0: no maps
+};
+
+__device__ __forceinline__ void tma_box_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                           unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // assembled 1D reference diagonal at node i of an axis with E elements (E == 0: degenerate axis)
@@ -483,7 +512,7 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
 // check and boundary weight is compile-time (measured: the predicate / select overhead of the
 // generic body is a visible share of K1's issue slots).
 template <int K, int Q, bool BLOCK, int EPI, bool FULL>
-__device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* smem) {
+__device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const SpkWsMaps& maps, double* smem) {
   using G = Geo<K, Q>;
   constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;
   constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
@@ -495,9 +524,9 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   double* dtab = MCs + 2 * G::MCBUF * G::MC_SZ;  // [(K+1)^3][DT_STRIDE] Jacobi table
   unsigned long long* ubar = reinterpret_cast<unsigned long long*>(dtab + G::DT_SZ);  // plane-buffer mbarriers
   unsigned long long* ibar = ubar + 2;  // split plane barrier (SPK_SPLIT_BAR)
-  // interior tiles load their planes with bulk-async copies (one per row, issued by warp 0) that
-  // complete on ubar[slot]; every other tile keeps the per-node cp.async path with zero-fill
-  constexpr bool BULK = FULL && SPK_BULK_LOAD;
+  // interior tiles load their planes with TMA boxes (issued by thread 0) that complete on
+  // ubar[slot]; every other tile keeps the per-node cp.async path with zero-fill
+  constexpr bool BULK = FULL && SPK_TMA_LOAD;
 
   const int tid = threadIdx.x;
   const SpkDims g = a.g;
@@ -566,66 +595,58 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // address, and one bit of `lzero` per item = zero-fill (slots outside the domain and, constrained,
   // y/z-boundary nodes). One 8-byte cp.async per item and plane whose ignore-src predicate writes
   // the zeros; no branches, no per-plane index math beyond one 64-bit add.
-  unsigned loff[G::LIT], ldst[G::LIT];
+  unsigned loff[BULK ? 1 : G::LIT], ldst[BULK ? 1 : G::LIT];
   unsigned lzero = 0u;
   unsigned lq[Q];  // virtual x-split: items of stage q (their global x is q*vplanes further)
 #pragma unroll
   for (int q = 0; q < Q; ++q) lq[q] = 0u;
   constexpr bool LTAIL = (G::LITEMS % NT) != 0;  // only the last item can be past the end
+  if constexpr (!BULK) {
 #pragma unroll
-  for (int i = 0; i < G::LIT; ++i) {
-    const int idx = min(tid + i * NT, G::LITEMS - 1);
-    const int q = idx / (NYin * NZin);
-    const int rem = idx - q * (NYin * NZin);
-    const int yy = rem / NZin, zz = rem - yy * NZin;
-    const int gy = y_lo - K + yy, gz = z_lo - K + zz;
-    const int slot = (q * NYin + yy) * NZp + zz;
-    ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
-    const bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
-    const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
-    loff[i] = (FULL || in) ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
-    if (!FULL && (!in || (a.constrained && bnd))) lzero |= 1u << i;
+    for (int i = 0; i < G::LIT; ++i) {
+      const int idx = min(tid + i * NT, G::LITEMS - 1);
+      const int q = idx / (NYin * NZin);
+      const int rem = idx - q * (NYin * NZin);
+      const int yy = rem / NZin, zz = rem - yy * NZin;
+      const int gy = y_lo - K + yy, gz = z_lo - K + zz;
+      const int slot = (q * NYin + yy) * NZp + zz;
+      ldst[i] = static_cast<unsigned>(__cvta_generic_to_shared(Us + slot));
+      const bool in = gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
+      const bool bnd = (!ydeg && (gy == 0 || gy == g.ny - 1)) || gz == 0 || gz == g.nz - 1;
+      loff[i] = (FULL || in) ? static_cast<unsigned>((q * a.su + (long long)gy * g.nz + gz) * 8) : 0u;
+      if (!FULL && (!in || (a.constrained && bnd))) lzero |= 1u << i;
 #pragma unroll
-    for (int qq = 0; qq < Q; ++qq)
-      if (q == qq) lq[qq] |= 1u << i;
+      for (int qq = 0; qq < Q; ++qq)
+        if (q == qq) lq[qq] |= 1u << i;
+    }
   }
   constexpr unsigned UBUF = G::U_SZ * sizeof(double);
 
-  // bulk descriptors: lane l of warp 0 copies rows l, l + 32, ...; per-row source element index
-  // (plane 0) and the parity of the row start for the Z-phase offset
-  constexpr int BRI = (G::BROWS + 31) / 32;
-  long long bsrc[BULK ? BRI : 1];
-  unsigned bpar0 = 0u;  // bit i: row start index parity at plane 0 (row = zoff of Z item i)
+  unsigned bpar0 = 0u;  // bit i: parity of Z item i's box start index at plane 0
   const unsigned podd = static_cast<unsigned>(plane_stride & 1);
-  if constexpr (BULK) {
-#pragma unroll
-    for (int i = 0; i < BRI; ++i) {
-      const int r = min(tid % 32 + 32 * i, G::BROWS - 1);
-      const int q = r / NYin, yy = r - q * NYin;
-      bsrc[i] = (long long)q * a.su + (long long)(y_lo - K + yy) * g.nz + (z_lo - K);
-    }
-  }
-  auto load_plane_bulk = [&](int x, auto BUF) {
+  auto load_plane_tma = [&](int x, auto BUF) {
     const unsigned buf = parity_of(BUF);
-    if (tid >= 32) return;
+    if (tid != 0) return;
     double* Ub = Us + buf * G::U_SZ;
-    if (tid == 0) mbar_arrive_expect_tx(&ubar[buf], G::BROWS * G::NZb * 8);
-    __syncwarp();
-    fence_proxy_async_smem();  // the buffer's previous generic-proxy readers are ordered before
+    mbar_arrive_expect_tx(&ubar[buf], G::TX_BYTES);
+    // loaded row yy is global row ye + yy and lives in box (yy & 1); the even map holds the even
+    // global rows (pair index gy / 2), the odd map the odd ones (pair index (gy - 1) / 2, + nz)
+    const int ye = y_lo - K;
+    const int r0e = (ye & 1) ? ye + 1 : ye, r0o = (ye & 1) ? ye : ye + 1;
+    const int c1e = r0e >> 1, c1o = (r0o - 1) >> 1;
+    const int be = (r0e - ye) & 1, bo = (r0o - ye) & 1;
+    const long long pb = (BLOCK ? (long long)b0 * a.su : 0) + maps.bias + (long long)x * plane_stride + (z_lo - K);
 #pragma unroll
-    for (int i = 0; i < BRI; ++i) {
-      const int r = tid + 32 * i;
-      if (r < G::BROWS) {
-        const double* src = u + bsrc[i] + (long long)x * plane_stride;
-        const uintptr_t al = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
-        bulk_g2s(Ub + r * G::NZb, reinterpret_cast<const void*>(al), G::NZb * 8, &ubar[buf]);
-      }
+    for (int q = 0; q < Q; ++q) {
+      const long long fe = pb + (long long)q * a.su, fo = fe + g.nz;
+      tma_box_2d(Ub + (q * 2 + be) * G::REG, &maps.even, (int)(fe & ~1LL), c1e, &ubar[buf]);
+      tma_box_2d(Ub + (q * 2 + bo) * G::REG, &maps.odd, (int)(fo & ~1LL), c1o, &ubar[buf]);
     }
   };
 
   auto load_plane = [&](int x, auto BUF) {
     if constexpr (BULK) {
-      load_plane_bulk(x, BUF);
+      load_plane_tma(x, BUF);
       return;
     }
     const unsigned buf = parity_of(BUF);
@@ -687,6 +708,8 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
       }
     }
   }
+  int zu[BULK ? G::ZIT : 1];  // TMA layout: offset of the item's box row in a plane buffer
+  unsigned zq = 0u;           // ... and its stage (2 bits per item: virtual x-split boundary planes)
   if constexpr (BULK) {
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
@@ -694,7 +717,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
       const long long e0 = (long long)q * a.su + (long long)(y_lo - K + yy) * g.nz + (z_lo - K);
       const uintptr_t addr = reinterpret_cast<uintptr_t>(u + e0);
       bpar0 |= static_cast<unsigned>((addr >> 3) & 1u) << i;
+      zu[i] = (q * 2 + (yy & 1)) * G::REG + (yy >> 1) * G::W;
+      zq |= static_cast<unsigned>(q) << (2 * i);
     }
+    static_assert(G::ZIT <= 16 && Q <= 4, "2 bits of stage per Z item");
   }
   // Y items: (q, z, segment of YS elements); lanes run along z
   int yoff[G::YIT], yeb[G::YIT];
@@ -721,13 +747,20 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
     const int ub = parity_of(PB), ab = ub;
     const double* Ub = Us + ub * G::U_SZ;
     double2* AB = reinterpret_cast<double2*>(ABs + ab * 2 * G::AB_SZ);
-    // constrained: the x-boundary planes are zero (bulk copies cannot zero-fill: their Z outputs are)
-    const bool xzero = BULK && a.constrained && (xp + g.x0 == 0 || xp + g.x0 == g.nxg - 1);
+    // constrained: the x-boundary planes are zero (the boxes hold the raw values: their Z outputs are
+    // zeroed; virtual x-split: per stage)
+    const bool vsp = BLOCK && a.vplanes != 0;
+    const bool xzero = BULK && a.constrained && !vsp && (xp + g.x0 == 0 || xp + g.x0 == g.nxg - 1);
     const unsigned pflip = BULK ? ((static_cast<unsigned>(xp) & podd) ? ~0u : 0u) : 0u;
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
       if (zeb[i] >= nez) continue;
-      const double* row = BULK ? Ub + zoff[i] * G::NZb + (((bpar0 ^ pflip) >> i) & 1u) : Ub + zoff[i] * NZp;
+      const double* row = BULK ? Ub + zu[BULK ? i : 0] + (((bpar0 ^ pflip) >> i) & 1u) : Ub + zoff[i] * NZp;
+      bool xz = xzero;
+      if (BULK && vsp && a.constrained) {
+        const int xgq = xp + g.x0 + static_cast<int>((zq >> (2 * i)) & 3u) * a.vplanes;
+        xz = xgq == 0 || xgq == g.nxg - 1;
+      }
       double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
       double L[K + 1], R[K + 1];
@@ -744,7 +777,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
           const double wl = (FULL || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
           double oa[K], ob[K];
           elem2<K>(cf, L, R, wl, wr, oa, ob);
-          if (BULK && xzero) {
+          if (BULK && xz) {
 #pragma unroll
             for (int r = 0; r < K; ++r) oa[r] = ob[r] = 0.0;
           }
@@ -955,6 +988,9 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   auto interval_split = [&](auto P, int t) {
     constexpr int p = decltype(P)::value;  // == t & 1
     if (t >= 1) mbar_wait(ibar, static_cast<unsigned>(t - 1) & 1u);
+    if constexpr (BULK) {
+      if (t < nplanes) mbar_wait(&ubar[p], static_cast<unsigned>(t >> 1) & 1u);
+    }
     if (t + 1 < nplanes) load_plane(xs + t + 1, IC<1 - p>{});
     if (t < nplanes) zphase(IC<p>{}, xs + t);
     if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{}, (t - 1) % 3);
@@ -989,7 +1025,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, double* 
   // instantiation except the stage-coupled k=2, Q=4 mix (C4's GMRES operator), whose doubled code
   // is slower (623 vs 575 us)
   constexpr bool UNROLL2 = BLOCK || !(K == 2 && Q == 4);
-  if constexpr (G::SPLIT && !BULK) {
+  if constexpr (G::SPLIT) {
     if (tid == 0) {
       mbar_init(ibar, NT);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1048,25 +1084,26 @@ template <int K, int Q, bool BLOCK, int EPI>
 __global__ void __launch_bounds__(Geo<K, Q>::NT,
                                   // (the fused Chebyshev epilogue spills at 64 registers: two CTAs)
                                   (EPI == EPI_CHEB && Geo<K, Q>::MINB > 2) ? 2 : Geo<K, Q>::MINB)
-    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a) {
-  extern __shared__ __align__(16) double smem[];
+    stage_apply_kernel(const __grid_constant__ SpkApplyArgs a, const __grid_constant__ SpkWsMaps maps) {
+  extern __shared__ __align__(128) double smem[];
   using G = Geo<K, Q>;
   if constexpr (SPK_FULL_TILES) {
     // the loaded rows are y in [K (ey0 - 1), K (ey0 + TYE)] (same for z): inside the domain, every
     // element of the tile real (ey0 >= 1, ey0 + TYE <= Ey), and away from the constrained boundary
     const SpkDims& g = a.g;
     const int ez0 = blockIdx.x * G::TZE, ey0 = blockIdx.y * G::TYE;
-    // (bulk loads: one more element on the high z side, since a row copy may read one double past
-    // the row's last loaded value; no virtual x-split)
-    const int lo = a.constrained ? 2 : 1, hi = (a.constrained || SPK_BULK_LOAD) ? 1 : 0;
+    // (TMA boxes may read one double past the tile's last loaded node: still inside the array, an
+    // interior tile never holds the array's last row; without tensor maps every tile takes the
+    // generic body)
+    const int lo = a.constrained ? 2 : 1, hi = a.constrained ? 1 : 0;
     const bool full = g.Ey > 0 && g.Ez > 0 && g.Ex > 0 && ey0 >= lo && ez0 >= lo && ey0 + G::TYE + hi <= g.Ey &&
-                      ez0 + G::TZE + hi <= g.Ez && !(SPK_BULK_LOAD && BLOCK && a.vplanes != 0);
+                      ez0 + G::TZE + hi <= g.Ez && (!SPK_TMA_LOAD || maps.bias >= 0);
     if (full) {
-      stage_apply_body<K, Q, BLOCK, EPI, true>(a, smem);
+      stage_apply_body<K, Q, BLOCK, EPI, true>(a, maps, smem);
       return;
     }
   }
-  stage_apply_body<K, Q, BLOCK, EPI, false>(a, smem);
+  stage_apply_body<K, Q, BLOCK, EPI, false>(a, maps, smem);
 }
 
 
@@ -1225,13 +1262,14 @@ __global__ void __launch_bounds__(256) small_apply_kernel(const __grid_constant_
 #include "stage_apply_ws.cuh"
 namespace {
 
-// K1w (stage_apply_ws.cuh) takes 3D launches on levels with at least SPK_WS_MIN nodes per axis
-// (SPK_WS=0: never)
+// K1w (stage_apply_ws.cuh), the warp-specialised variant, is a measured alternative and off by
+// default (profiles/r02_k1w_*: C2 432 vs 399 us): SPK_WS=1 routes 3D launches on levels with at
+// least SPK_WS_MIN nodes per axis to it
 inline int spk_ws_min_nodes() {
   static int v = -2;
   if (v == -2) {
     const char* e = std::getenv("SPK_WS");
-    if (e && e[0] == '0') v = -1;
+    if (!e || e[0] != '1') v = -1;
     else {
       const char* m = std::getenv("SPK_WS_MIN");
       v = m ? std::atoi(m) : 0;
@@ -1311,12 +1349,13 @@ cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out)
       return spk_launch(small_apply_kernel<K, EPI, false>, grid, dim3(256), 0, s, a);
     }
   }
+  SpkWsMaps maps;
+  const bool have_maps = SPK_TMA_LOAD && ws_maps<K, Q>(a, BLOCK, &maps);
+  if (!have_maps) maps.bias = -1;
   if constexpr (EPI != EPI_DINV) {
     const int wsmin = spk_ws_min_nodes();
-    if (wsmin >= 0 && a.g.nz >= wsmin) {
-      SpkWsMaps maps;
-      if (ws_maps<K, Q>(a, BLOCK, &maps)) return launch_ws<K, Q, BLOCK, EPI>(a, maps, s, nctas_out);
-    }
+    if (have_maps && wsmin >= 0 && a.g.nz >= wsmin && a.vplanes == 0)
+      return launch_ws<K, Q, BLOCK, EPI>(a, maps, s, nctas_out);
   }
   const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
   static bool configured = false;
@@ -1333,7 +1372,7 @@ cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out)
   if (((long long)(Q - 1) * a.su + a.g.n) * 8 > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
   dim3 grid(gz, gy, a.nchunks * nb);
   if (nctas_out) *nctas_out = gz * gy * a.nchunks * nb;
-  return spk_launch(kern, grid, dim3(G::NT), smem, s, a);
+  return spk_launch(kern, grid, dim3(G::NT), smem, s, a, maps);
 }
 
 #define SPK_EPIS(K, Q, B)                                                   \

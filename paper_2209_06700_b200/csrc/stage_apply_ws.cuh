@@ -56,15 +56,7 @@ template <int K, int Q> struct WGeo {
   static constexpr int NXW = SPK_WS_NXW;  // X warps: 256 / (32 NXW) tile nodes per thread
   static constexpr int NT = 32 * (NZW + NYW + 1 + NXW);
   static constexpr int YW0 = NZW, PW = NZW + NYW, XW0 = NZW + NYW + 1;
-  // box width: even (16-byte multiple), >= NZin + 1 (odd-row skew), W / 2 odd (bank spread)
-  static constexpr int wpitch() {
-    int w = (NZin + 2) & ~1;
-    while ((w / 2) % 2 == 0) w += 2;
-    return w;
-  }
-  static constexpr int W = wpitch();
-  static constexpr int BOXR = (NYin + 1) / 2;
-  static constexpr int REG = (BOXR * W + 15) / 16 * 16;  // one box, 128-byte multiple
+  static constexpr int W = G::W, BOXR = G::BOXR, REG = G::REG;  // TMA boxes: see Geo
   static constexpr int U_SLOT = Q * 2 * REG;             // doubles
   static constexpr int AB_SLOT = 2 * Q * NYin * TZp;
   static constexpr int MC_SLOT = 2 * Q * TY * TZp;
@@ -95,35 +87,15 @@ template <int K, int Q> struct WGeo {
   static constexpr unsigned TX_BYTES = 2u * Q * BOXR * W * 8u;
 };
 
-struct SpkWsMaps {
-  CUtensorMap even, odd;
-  int bias;  // elements between the 16-byte aligned map base and args.u (0 or 1)
-};
-
 // named barriers (producer / consumer between roles: the waiting warps block in hardware instead of
 // polling an mbarrier; ids 1..15, count = arriving + waiting threads)
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
+// (the documented PTX producer pattern: st.shared ; bar.arrive  /  bar.sync ; ld.shared -- the
+// barrier orders the participating threads' prior shared-memory accesses)
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
-  // (the documented PTX producer pattern: st.shared ; bar.arrive  /  bar.sync ; ld.shared -- the
-  // barrier orders the participating threads' prior shared-memory accesses; an explicit membar.cta
-  // in front cost ~100-300 cycles per arrive with stores in flight)
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
-}
-// reference-element tables as constant-bank operands of the DFMAs (no registers, no moves)
-template <int K> struct CT {
-  __device__ static __forceinline__ double M(int r, int s2) { return c_hat[K - 1][0][r][s2]; }
-  __device__ static __forceinline__ double S(int r, int s2) { return c_hat[K - 1][1][r][s2]; }
-};
-
-__device__ __forceinline__ void tma_box_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                           unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
 }
 
 template <int K, int Q, bool BLOCK, int EPI, bool FULL>
@@ -622,9 +594,10 @@ inline SpkEncodeTiled spk_encode_tiled() {
 // whether K1w can take this launch, and its tensor maps
 template <int K, int Q>
 bool ws_maps(const SpkApplyArgs& a, bool block, SpkWsMaps* m) {
-  using G = WGeo<K, Q>;
+  using G = Geo<K, Q>;
   const SpkDims& g = a.g;
-  if (g.Ex <= 0 || g.Ey <= 0 || g.Ez <= 0 || a.vplanes != 0) return false;
+  m->bias = -1;
+  if (g.Ex <= 0 || g.Ey <= 0 || g.Ez <= 0) return false;
   SpkEncodeTiled enc = spk_encode_tiled();
   if (!enc) return false;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(a.u);
