@@ -45,6 +45,7 @@ struct spk_ctx {
   // fused CHEB variants spill at 128 registers). Measured: C1 (2 blocks, tiny levels) prefers fused,
   // C3 / C4 (3-4 blocks) split on every level, single-block V-cycles split from ~2^18 DoFs.
   long long split_cheb_min = 1LL << 18;
+  int split_cheb_nblk = 3;  // (SPK_CHEB_SPLIT_NBLK)
   int per_cta2_epi = 1;   // epilogues (bit mask over SpkEpi) that take the two-per-CTA launch (SPK_PER_CTA2_EPI)
   int vsplit_v = 0;       // virtual x-ranges per CTA of a single-block launch (SPK_VSPLIT_V: 4 or 2; 0: automatic)
   // blocks swept together by one K1 CTA (SPK_PER_CTA_MAX; 0: two per CTA where SPK_PER_CTA2_* allow.
@@ -345,7 +346,7 @@ bool cheb_split(const spk_ctx* c, int level, int nblk) {
   // levels the direct small-level kernel takes (one CTA row per block) always fuse: there a launch
   // costs more than the epilogue's loads
   if (small_level(c, level)) return false;
-  return nblk >= 3 || (long long)nblk * c->dims[level].n >= c->split_cheb_min;
+  return nblk >= c->split_cheb_nblk || (long long)nblk * c->dims[level].n >= c->split_cheb_min;
 }
 
 }  // namespace
@@ -385,6 +386,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
     return fail(SPK_ECONFIG, "max_level must be in [1, 10], got " + std::to_string(max_level));
   spk_ctx* c = new spk_ctx();
   if (const char* e = std::getenv("SPK_CHEB_SPLIT")) c->split_cheb_min = std::atoll(e);  // tuning override
+  if (const char* e = std::getenv("SPK_CHEB_SPLIT_NBLK")) c->split_cheb_nblk = std::atoi(e);
   if (const char* e = std::getenv("SPK_VSPLIT")) c->vsplit = std::atoi(e);
   if (const char* e = std::getenv("SPK_PER_CTA_MAX")) c->per_cta_max = std::max(0, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("SPK_PER_CTA2_EPI")) c->per_cta2_epi = std::atoi(e);

@@ -128,8 +128,8 @@ template <int K, int Q> struct Geo {
 #ifndef SPK_MINB4
 #define SPK_MINB4 3
 #endif
-  static constexpr int MINB = (SPK_MINB4 && K <= SPK_MINB4 && NT <= 256 && SMEM_DOUBLES * 8 <= 55 * 1024) ? 4
-                              : (NT <= 192 && SMEM_DOUBLES * 8 <= 74 * 1024)   ? 3
+  static constexpr bool MINB4_OK = SPK_MINB4 && K <= SPK_MINB4 && NT <= 256 && SMEM_DOUBLES * 8 <= 55 * 1024;
+  static constexpr int MINB = (NT <= 192 && SMEM_DOUBLES * 8 <= 74 * 1024)   ? 3
                               : (NT <= 256 && SMEM_DOUBLES * 8 <= 112 * 1024) ? 2
                                                                               : 1;
 };
@@ -1082,8 +1082,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
 
 template <int K, int Q, bool BLOCK, int EPI>
 __global__ void __launch_bounds__(Geo<K, Q>::NT,
-                                  // (the fused Chebyshev epilogue spills at 64 registers: two CTAs)
-                                  (EPI == EPI_CHEB && Geo<K, Q>::MINB > 2) ? 2 : Geo<K, Q>::MINB)
+                                  // (block mode only, and not the fused Chebyshev epilogue, which spills at
+                                  // 64 registers; the pair mode's 2x2 epilogues lose at four CTAs:
+                                  // measured C5-gmg 75.8 -> 84.2 ms / step)
+                                  (Geo<K, Q>::MINB4_OK && BLOCK && EPI != EPI_CHEB) ? 4 : Geo<K, Q>::MINB)
     stage_apply_kernel(const __grid_constant__ SpkApplyArgs a, const __grid_constant__ SpkWsMaps maps) {
   extern __shared__ __align__(128) double smem[];
   using G = Geo<K, Q>;
