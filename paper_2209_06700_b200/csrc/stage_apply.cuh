@@ -710,6 +710,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   }
   int zu[BULK ? G::ZIT : 1];  // TMA layout: offset of the item's box row in a plane buffer
   unsigned zq = 0u;           // ... and its stage (2 bits per item: virtual x-split boundary planes)
+  unsigned zfl = 0u;          // ... and its constrained-boundary masks (3 bits per item)
   if constexpr (BULK) {
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
@@ -719,8 +720,17 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       bpar0 |= static_cast<unsigned>((addr >> 3) & 1u) << i;
       zu[i] = (q * 2 + (yy & 1)) * G::REG + (yy >> 1) * G::W;
       zq |= static_cast<unsigned>(q) << (2 * i);
+      // constrained operator on a tile next to the boundary: the boxes hold the raw boundary values,
+      // which the operator treats as zero -- a boundary ROW zeroes its Z outputs, a boundary NODE
+      // at the low / high end of the loaded z range is dropped from its element
+      if (a.constrained && zeb[i] < TZE) {
+        const int gy = y_lo - K + yy;
+        if (gy == 0 || gy == g.ny - 1) zfl |= 1u << (3 * i);
+        if (z_lo - K == 0 && zeb[i] == 0) zfl |= 2u << (3 * i);
+        if (z_lo + TZ == g.nz - 1 && zeb[i] + G::ZS >= TZE) zfl |= 4u << (3 * i);
+      }
     }
-    static_assert(G::ZIT <= 16 && Q <= 4, "2 bits of stage per Z item");
+    static_assert(G::ZIT <= 10 && Q <= 4, "2 bits of stage, 3 mask bits per Z item");
   }
   // Y items: (q, z, segment of YS elements); lanes run along z
   int yoff[G::YIT], yeb[G::YIT];
@@ -761,11 +771,14 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
         const int xgq = xp + g.x0 + static_cast<int>((zq >> (2 * i)) & 3u) * a.vplanes;
         xz = xgq == 0 || xgq == g.nxg - 1;
       }
+      const unsigned fl = BULK ? (zfl >> (3 * i)) & 7u : 0u;
+      if (BULK && (fl & 1u)) xz = true;
       double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
       double L[K + 1], R[K + 1];
 #pragma unroll
       for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
+      if (BULK && (fl & 2u)) L[0] = 0.0;
 #pragma unroll
       for (int el = 0; el < G::ZS; ++el) {
         const int e = e_beg + el;
@@ -773,6 +786,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
           R[0] = L[K];
 #pragma unroll
           for (int s = 1; s <= K; ++s) R[s] = row[K * e + K + s];
+          if (BULK && (fl & 4u) && e == TZE - 1) R[K] = 0.0;
           const int ez = ez0 + e;
           const double wl = (FULL || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
           double oa[K], ob[K];
@@ -1097,7 +1111,10 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT,
     // (TMA boxes may read one double past the tile's last loaded node: still inside the array, an
     // interior tile never holds the array's last row; without tensor maps every tile takes the
     // generic body)
-    const int lo = a.constrained ? 2 : 1, hi = a.constrained ? 1 : 0;
+    // (constrained: with the TMA boxes a tile next to the boundary masks the loaded boundary row /
+    // node in its Z sweep, so it is still an interior tile)
+    const bool tma = SPK_TMA_LOAD && maps.bias >= 0;
+    const int lo = (a.constrained && !tma) ? 2 : 1, hi = (a.constrained && !tma) ? 1 : 0;
     const bool full = g.Ey > 0 && g.Ez > 0 && g.Ex > 0 && ey0 >= lo && ez0 >= lo && ey0 + G::TYE + hi <= g.Ey &&
                       ez0 + G::TZE + hi <= g.Ez && (!SPK_TMA_LOAD || maps.bias >= 0);
     if (full) {
