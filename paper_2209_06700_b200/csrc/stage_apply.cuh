@@ -38,6 +38,9 @@
 #define SPK_SPLIT_BAR 1
 #endif
 // TMA plane loads for interior tiles (two 2D boxes per stage and plane, see load_plane_tma)
+#ifndef SPK_WARP_ARRIVE
+#define SPK_WARP_ARRIVE 0   // measured: no gain (C2 388.3 vs 387.8 us)
+#endif
 #ifndef SPK_TMA_LOAD
 #define SPK_TMA_LOAD 1
 #endif
@@ -511,8 +514,11 @@ __device__ __forceinline__ void epilogue(const SpkApplyArgs& a, int b0, const do
 // slots, no missing neighbour elements, no constrained y/z boundary rows): every per-item bound
 // check and boundary weight is compile-time (measured: the predicate / select overhead of the
 // generic body is a visible share of K1's issue slots).
-template <int K, int Q, bool BLOCK, int EPI, bool FULL>
+// FULLV: 0 generic tile; 1 interior tile; 2 interior tile on the low y / z boundary (the missing
+// element gets weight 0 in the Z / Y sweeps, boundary rows are identity rows in the epilogue)
+template <int K, int Q, bool BLOCK, int EPI, int FULLV>
 __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const SpkWsMaps& maps, double* smem) {
+  constexpr bool FULL = FULLV != 0, LOW = FULLV == 2;
   using G = Geo<K, Q>;
   constexpr int TYE = G::TYE, TZE = G::TZE, TY = G::TY, TZ = G::TZ, NT = G::NT;
   constexpr int NYin = G::NYin, NZin = G::NZin, NZp = G::NZp, TZp = G::TZp;
@@ -710,7 +716,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   }
   int zu[BULK ? G::ZIT : 1];  // TMA layout: offset of the item's box row in a plane buffer
   unsigned zq = 0u;           // ... and its stage (2 bits per item: virtual x-split boundary planes)
-  unsigned zfl = 0u;          // ... and its constrained-boundary masks (3 bits per item)
+  unsigned zfl = 0u;          // ... and its boundary masks (5 bits per item)
   if constexpr (BULK) {
 #pragma unroll
     for (int i = 0; i < G::ZIT; ++i) {
@@ -725,12 +731,15 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       // at the low / high end of the loaded z range is dropped from its element
       if (a.constrained && zeb[i] < TZE) {
         const int gy = y_lo - K + yy;
-        if (gy == 0 || gy == g.ny - 1) zfl |= 1u << (3 * i);
-        if (z_lo - K == 0 && zeb[i] == 0) zfl |= 2u << (3 * i);
-        if (z_lo + TZ == g.nz - 1 && zeb[i] + G::ZS >= TZE) zfl |= 4u << (3 * i);
+        if (gy == 0 || gy == g.ny - 1) zfl |= 1u << (5 * i);
+        // (node z = 0 is the first loaded node of a tile one element in, or the first node of
+        // element 0 = the left-element node 0 of an item that starts at element 1)
+        if ((z_lo - K == 0 && zeb[i] == 0) || (ez0 == 0 && zeb[i] == 1)) zfl |= 2u << (5 * i);
+        if (z_lo + TZ == g.nz - 1 && zeb[i] + G::ZS >= TZE) zfl |= 4u << (5 * i);
+        if (ez0 == 0 && zeb[i] == 0) zfl |= 16u << (5 * i);  // node z = 0 is the first node of element 0
       }
     }
-    static_assert(G::ZIT <= 10 && Q <= 4, "2 bits of stage, 3 mask bits per Z item");
+    static_assert(G::ZIT <= 6 && Q <= 4, "2 bits of stage, 5 mask bits per Z item");
   }
   // Y items: (q, z, segment of YS elements); lanes run along z
   int yoff[G::YIT], yeb[G::YIT];
@@ -771,7 +780,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
         const int xgq = xp + g.x0 + static_cast<int>((zq >> (2 * i)) & 3u) * a.vplanes;
         xz = xgq == 0 || xgq == g.nxg - 1;
       }
-      const unsigned fl = BULK ? (zfl >> (3 * i)) & 7u : 0u;
+      const unsigned fl = BULK ? (zfl >> (5 * i)) & 31u : 0u;
       if (BULK && (fl & 1u)) xz = true;
       double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
@@ -787,8 +796,11 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
 #pragma unroll
           for (int s = 1; s <= K; ++s) R[s] = row[K * e + K + s];
           if (BULK && (fl & 4u) && e == TZE - 1) R[K] = 0.0;
+          if (BULK && (fl & 16u) && el == 0) R[0] = 0.0;
           const int ez = ez0 + e;
-          const double wl = (FULL || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
+          // (interior tiles may sit on the low boundary: element -1 does not exist, its slots hold
+          // finite values of the neighbouring row or TMA zeros and get weight 0)
+          const double wl = ((FULL && !LOW) || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
           double oa[K], ob[K];
           elem2<K>(cf, L, R, wl, wr, oa, ob);
           if (BULK && xz) {
@@ -846,7 +858,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
             Rb[s] = t.y;
           }
           const int ey = ey0 + e;
-          const double wl = (FULL || ey > 0) ? 1.0 : 0.0, wr = (FULL || ey < g.Ey) ? 1.0 : 0.0;
+          const double wl = ((FULL && !LOW) || ey > 0) ? 1.0 : 0.0, wr = (FULL || ey < g.Ey) ? 1.0 : 0.0;
           double om[K], oc[K];
           elem3<K>(cf, La, Ra, Lb, Rb, wl, wr, om, oc);
 #pragma unroll
@@ -941,7 +953,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       }
       const int y = y_lo + yl, z = z_lo + zl;
       if (xdeg) {
-        epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, 0, y, z, (long long)pyz[j], pq, sumsq);
+        epilogue<K, Q, BLOCK, EPI, FULL && !LOW>(a, b0, lamq, dtab, ith, 0, y, z, (long long)pyz[j], pq, sumsq);
         continue;
       }
 #pragma unroll
@@ -957,7 +969,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
 #pragma unroll
             for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
             const int xx = K * ecur + s;
-            epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, xx, y, z,
+            epilogue<K, Q, BLOCK, EPI, FULL && !LOW>(a, b0, lamq, dtab, ith, xx, y, z,
                                        (long long)xx * plane_stride + pyz[j], val, sumsq);
           }
         }
@@ -966,7 +978,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
 #pragma unroll
           for (int q = 0; q < Q; ++q) val[q] = acc[j][q][K];
           // virtual x-split: only the last range owns it (the others' is the next range's plane 0)
-          epilogue<K, Q, BLOCK, EPI, FULL>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
+          epilogue<K, Q, BLOCK, EPI, FULL && !LOW>(a, b0, lamq, dtab, ith, K * g.Ex, y, z,
                                      (long long)(K * g.Ex) * plane_stride + pyz[j], val, sumsq,
                                      (BLOCK && a.vplanes) ? Q - 1 : 0);
         }
@@ -1009,7 +1021,14 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
     if (t < nplanes) zphase(IC<p>{}, xs + t);
     if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{}, (t - 1) % 3);
     cp_async_wait_all();  // this thread's part of plane t+1 has landed
-    mbar_arrive(ibar);
+    if constexpr (SPK_WARP_ARRIVE) {
+      // one arrival per warp: every arrival wakes the threads sleeping in the barrier wait
+      // (NANOSLEEP.SYNCS), so 8 arrivals per phase cost the waiters fewer polls than 256
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(ibar);
+    } else {
+      mbar_arrive(ibar);
+    }
     if (t >= 2) xphase(xs + t - 2, (t - 2) % 3);
   };
   auto interval = [&](auto P, int t) {
@@ -1041,7 +1060,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   constexpr bool UNROLL2 = BLOCK || !(K == 2 && Q == 4);
   if constexpr (G::SPLIT) {
     if (tid == 0) {
-      mbar_init(ibar, NT);
+      mbar_init(ibar, SPK_WARP_ARRIVE ? NT / 32 : NT);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     cp_async_wait_all();
@@ -1114,15 +1133,18 @@ __global__ void __launch_bounds__(Geo<K, Q>::NT,
     // (constrained: with the TMA boxes a tile next to the boundary masks the loaded boundary row /
     // node in its Z sweep, so it is still an interior tile)
     const bool tma = SPK_TMA_LOAD && maps.bias >= 0;
-    const int lo = (a.constrained && !tma) ? 2 : 1, hi = (a.constrained && !tma) ? 1 : 0;
+    // (low boundary: rows below the plane are TMA zeros, the missing element gets weight 0 in the
+    // Z / Y sweeps; only the ragged tiles on the high side take the generic body)
+    const int lo = tma ? 0 : (a.constrained ? 2 : 1), hi = (a.constrained && !tma) ? 1 : 0;
     const bool full = g.Ey > 0 && g.Ez > 0 && g.Ex > 0 && ey0 >= lo && ez0 >= lo && ey0 + G::TYE + hi <= g.Ey &&
                       ez0 + G::TZE + hi <= g.Ez && (!SPK_TMA_LOAD || maps.bias >= 0);
     if (full) {
-      stage_apply_body<K, Q, BLOCK, EPI, true>(a, maps, smem);
+      if (ey0 == 0 || ez0 == 0) stage_apply_body<K, Q, BLOCK, EPI, 2>(a, maps, smem);
+      else stage_apply_body<K, Q, BLOCK, EPI, 1>(a, maps, smem);
       return;
     }
   }
-  stage_apply_body<K, Q, BLOCK, EPI, false>(a, maps, smem);
+  stage_apply_body<K, Q, BLOCK, EPI, 0>(a, maps, smem);
 }
 
 
