@@ -44,6 +44,10 @@
 #ifndef SPK_TMA_LOAD
 #define SPK_TMA_LOAD 1
 #endif
+// EPI_STORE elements without identity rows are written with plain streaming stores (no per-node tests)
+#ifndef SPK_FAST_STORE
+#define SPK_FAST_STORE 1
+#endif
 
 namespace {
 
@@ -209,15 +213,33 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// (with a suspend-time hint the waiting thread sleeps in the barrier instead of re-polling: the
-// polling loop was ~11 % of K1's issued instructions, profiles/r02_stage_apply_ncu_summary.txt)
+// Waiting on an mbarrier costs issue slots: K1 is bound by its non-DFMA instructions (the FP64 pipe
+// takes a DFMA every other cycle per scheduler and ~1 other instruction per DFMA is free, tools/
+// ubench/fp64_mix.cu), and try_wait with a suspend-time hint still woke the waiting warps ~15 times
+// per wait (17 % of K1's issued instructions were its polling loop: profiles/r02_k1_final_ncu.txt).
+// SPK_WAIT_NS > 0: test once, then sleep SPK_WAIT_NS between tests.
+#ifndef SPK_WAIT_NS
+#define SPK_WAIT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+#if SPK_WAIT_NS > 0
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SPK_MBAR_WAIT_%=:\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @p bra SPK_MBAR_DONE_%=;\n"
+      " nanosleep.u32 %2;\n"
+      " bra SPK_MBAR_WAIT_%=;\n"
+      "SPK_MBAR_DONE_%=:\n}\n" ::"r"(smem_u32(bar)), "r"(phase), "r"((unsigned)SPK_WAIT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "SPK_MBAR_WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra SPK_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase), "r"(0x989680u)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -963,14 +985,31 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       if (r_loc == K) {
         // element ecur complete: nodes K*ecur + s, s < K
         if (ecur >= ex0) {
+          // plain stores (CTA-uniform test): nothing of this element is a constrained identity row
+          // -- unconstrained operator, or an interior tile away from the x = 0 plane -- so the
+          // generic epilogue's per-node boundary tests and 64-bit index products are skipped
+          bool fast = false;
+          if constexpr (EPI == EPI_STORE && SPK_FAST_STORE)
+            fast = !(BLOCK && a.vplanes != 0) &&
+                   (!a.constrained || (FULL && !LOW && K * ecur + g.x0 != 0));
+          if (fast) {
+            double* vp = a.v + (BLOCK ? (long long)b0 * a.sv : 0) + (long long)(K * ecur) * plane_stride + pyz[j];
 #pragma unroll
-          for (int s = 0; s < K; ++s) {
-            double val[Q];
+            for (int s = 0; s < K; ++s) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
-            const int xx = K * ecur + s;
-            epilogue<K, Q, BLOCK, EPI, FULL && !LOW>(a, b0, lamq, dtab, ith, xx, y, z,
-                                       (long long)xx * plane_stride + pyz[j], val, sumsq);
+              for (int q = 0; q < Q; ++q) __stcs(vp + q * a.sv, acc[j][q][s]);
+              vp += plane_stride;
+            }
+          } else {
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+              double val[Q];
+#pragma unroll
+              for (int q = 0; q < Q; ++q) val[q] = acc[j][q][s];
+              const int xx = K * ecur + s;
+              epilogue<K, Q, BLOCK, EPI, FULL && !LOW>(a, b0, lamq, dtab, ith, xx, y, z,
+                                         (long long)xx * plane_stride + pyz[j], val, sumsq);
+            }
           }
         }
         if (ecur + 1 == g.Ex && a.store_last) {  // final vertex plane nx-1 (left element only)
