@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <type_traits>
 #include "spk_internal.cuh"
 #include "spk_tables.cuh"
 #include <cuda.h>
@@ -43,6 +44,29 @@
 #endif
 #ifndef SPK_TMA_LOAD
 #define SPK_TMA_LOAD 1
+#endif
+// Balanced Z map (k = 4, Q = 3, 256 threads): the 192 Y items occupy six of the eight warps, so with
+// one Z item per thread the two Y-less warps idle for ~40 % of every plane interval. Here the Y-less
+// warps take two whole Z items each and the other Z items are split into half-element items (output
+// rows {0, 1} / {2, 3}) spread over the six Y warps: per-warp DFMA work per interval 159 / 164 / 170
+// instead of 105 / 184.
+// MEASURED AND REJECTED (off): bitwise identical results, barrier waits down (long-scoreboard stall
+// 1.06 -> 0.84 per issue), but C2 went 365 -> 466 us: warps of one scheduler now run different Z code
+// and miss in the instruction cache (no_instruction stall 0.36 -> 1.37 per issue), even with the
+// smaller runtime-index X-phase (424 us). profiles/r02_k1_ab.txt
+#ifndef SPK_ZBAL
+#define SPK_ZBAL 0
+#endif
+// K1's hot loop is large enough to miss in the instruction cache (ncu: no_instruction stalls); knobs
+// that trade compile-time constants for footprint
+#ifndef SPK_SPLIT_UNROLL2
+#define SPK_SPLIT_UNROLL2 1
+#endif
+// (measured: one interval copy with runtime buffer parity loses, C2 369 -> 387 us; one X-phase copy
+// with the x-table column read from constant memory by the plane index wins, C2 369 -> 364 us,
+// constrained 415 -> 404 us)
+#ifndef SPK_XR_RUNTIME
+#define SPK_XR_RUNTIME 1
 #endif
 // EPI_STORE elements without identity rows are written with plain streaming stores (no per-node tests)
 #ifndef SPK_FAST_STORE
@@ -116,6 +140,9 @@ template <int K, int Q> struct Geo {
   static constexpr int ZSEG = (TZE + ZS - 1) / ZS;
   static constexpr int ZITEMS = Q * NYin * ZSEG;
   static constexpr int ZIT = (ZITEMS + NT - 1) / NT;
+  // balanced Z map (SPK_ZBAL): two item slots per thread, each a whole item or a half item
+  static constexpr bool ZBAL = SPK_ZBAL && K == 4 && Q == 3 && NT == 256 && ZS == 1 && TYE == 4 && TZE == 4;
+  static constexpr int ZSLOTS = ZBAL ? 2 : ZIT;
   // Y items: (q, z, element segment)
 #ifdef SPK_YS
   static constexpr int YS = (Q >= 2) ? SPK_YS : 1;
@@ -190,6 +217,8 @@ template <int V> struct IC { static constexpr int value = V; };
 // plane-buffer parity: a compile-time IC<p> (unrolled pipeline) or a runtime int
 template <int V> __device__ __forceinline__ constexpr int parity_of(IC<V>) { return V; }
 __device__ __forceinline__ int parity_of(int v) { return v; }
+template <int V> __device__ __forceinline__ constexpr IC<1 - V> other_parity(IC<V>) { return {}; }
+__device__ __forceinline__ int other_parity(int v) { return 1 - v; }
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -364,6 +393,37 @@ __device__ __forceinline__ void elem2(const Coef<K>& cf, const double (&L)[K + 1
     }
     o1[r] = a1;
     o2[r] = a2;
+  }
+}
+
+// half-element forms of elem2 (balanced Z map): FIRST = output rows [0, K/2) (the vertex row needs the
+// left element), !FIRST = rows [K/2, K) (right element only); outputs land in o1 / o2 [0, K/2)
+template <int K, bool FIRST>
+__device__ __forceinline__ void elem2_half(const Coef<K>& cf, const double (&L)[K + 1], const double (&R)[K + 1],
+                                           double wl, double wr, double (&o1)[K / 2], double (&o2)[K / 2]) {
+  constexpr int H = K / 2;
+  if constexpr (FIRST) {
+    double l1 = 0.0, l2 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      l1 = fma(cf.m(K, s), L[s], l1);
+      l2 = fma(cf.s(K, s), L[s], l2);
+      r1 = fma(cf.m(0, s), R[s], r1);
+      r2 = fma(cf.s(0, s), R[s], r2);
+    }
+    o1[0] = fma(wl, l1, wr * r1);
+    o2[0] = fma(wl, l2, wr * r2);
+  }
+#pragma unroll
+  for (int r = FIRST ? 1 : H; r < (FIRST ? H : K); ++r) {
+    double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int s = 0; s <= K; ++s) {
+      a1 = fma(cf.m(r, s), R[s], a1);
+      a2 = fma(cf.s(r, s), R[s], a2);
+    }
+    o1[FIRST ? r : r - H] = a1;
+    o2[FIRST ? r : r - H] = a2;
   }
 }
 
@@ -705,18 +765,32 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   };
 
   // Z items: (q, yy, segment of ZS elements); lanes run along yy (odd pitch -> no bank conflicts)
-  int zoff[G::ZIT], zeb[G::ZIT];
+  constexpr int ZSL = G::ZSLOTS;
+  int zoff[ZSL], zeb[ZSL];
+  unsigned zpart = 0u;  // balanced map: 2 bits per slot -- 0 whole item, 1 rows {0,1}, 2 rows {2,3}
 #pragma unroll
-  for (int i = 0; i < G::ZIT; ++i) {
-    const int it = tid + i * NT;
+  for (int i = 0; i < ZSL; ++i) {
     zeb[i] = TZE;  // inactive
     zoff[i] = 0;
-    if (it < G::ZITEMS) {
-      // item order: first rows 0..15 of every (q, segment) -- whole half-warps on one segment, so
-      // the odd row pitch makes them conflict-free -- then the remaining rows, row-major across
-      // (q, segment) (the mixed half-warps that remain are conflict-free for these pitches too)
-      constexpr int R = NYin < 16 ? NYin : 16;
-      constexpr int QS = Q * G::ZSEG;
+    // item order: first rows 0..15 of every (q, segment) -- whole half-warps on one segment, so
+    // the odd row pitch makes them conflict-free -- then the remaining rows, row-major across
+    // (q, segment) (the mixed half-warps that remain are conflict-free for these pitches too)
+    constexpr int R = NYin < 16 ? NYin : 16;
+    constexpr int QS = Q * G::ZSEG;
+    constexpr int T = QS * (NYin - R);
+    int it = tid + i * NT;  // position in the item order; -1: none
+    if constexpr (G::ZBAL) {
+      // warps 0, 1 (no Y items): two whole head items; warps 2, 3: first halves of the other head
+      // items; warps 4, 5: first halves of the tail items; warps 6, 7: the second halves of both
+      const int w2 = tid >> 6, l = tid & 63;
+      unsigned part = 0u;
+      if (w2 == 0) it = l + 64 * i;
+      else if (w2 == 1) { it = i == 0 ? 128 + l : -1; part = 1u; }
+      else if (w2 == 2) { it = (i == 0 && l < T) ? QS * R + l : -1; part = 1u; }
+      else { it = i == 0 ? 128 + l : (l < T ? QS * R + l : -1); part = 2u; }
+      zpart |= part << (2 * i);
+    }
+    if (it >= 0 && it < G::ZITEMS) {
       int yy, qs;
       if (it < QS * R) {
         qs = it / R;
@@ -724,7 +798,6 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       } else {
         // rows past the first 16: the launcher's order (ztail_order), in which every 8 consecutive
         // lanes write 8 distinct 16-byte slots of the (A, B) buffer
-        constexpr int T = QS * (NYin - R);
         const int idx = T <= SPK_ZTAIL_MAX ? static_cast<int>(a.ztail[it - QS * R]) : it - QS * R;
         yy = R + idx / QS;
         qs = idx - (yy - R) * QS;
@@ -736,12 +809,12 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       }
     }
   }
-  int zu[BULK ? G::ZIT : 1];  // TMA layout: offset of the item's box row in a plane buffer
+  int zu[BULK ? ZSL : 1];  // TMA layout: offset of the item's box row in a plane buffer
   unsigned zq = 0u;           // ... and its stage (2 bits per item: virtual x-split boundary planes)
   unsigned zfl = 0u;          // ... and its boundary masks (5 bits per item)
   if constexpr (BULK) {
 #pragma unroll
-    for (int i = 0; i < G::ZIT; ++i) {
+    for (int i = 0; i < ZSL; ++i) {
       const int q = zoff[i] / NYin, yy = zoff[i] - q * NYin;
       const long long e0 = (long long)q * a.su + (long long)(y_lo - K + yy) * g.nz + (z_lo - K);
       const uintptr_t addr = reinterpret_cast<uintptr_t>(u + e0);
@@ -761,7 +834,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
         if (ez0 == 0 && zeb[i] == 0) zfl |= 16u << (5 * i);  // node z = 0 is the first node of element 0
       }
     }
-    static_assert(G::ZIT <= 6 && Q <= 4, "2 bits of stage, 5 mask bits per Z item");
+    static_assert(ZSL <= 6 && Q <= 4, "2 bits of stage, 5 mask bits per Z item");
   }
   // Y items: (q, z, segment of YS elements); lanes run along z
   int yoff[G::YIT], yeb[G::YIT];
@@ -794,7 +867,7 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
     const bool xzero = BULK && a.constrained && !vsp && (xp + g.x0 == 0 || xp + g.x0 == g.nxg - 1);
     const unsigned pflip = BULK ? ((static_cast<unsigned>(xp) & podd) ? ~0u : 0u) : 0u;
 #pragma unroll
-    for (int i = 0; i < G::ZIT; ++i) {
+    for (int i = 0; i < ZSL; ++i) {
       if (zeb[i] >= nez) continue;
       const double* row = BULK ? Ub + zu[BULK ? i : 0] + (((bpar0 ^ pflip) >> i) & 1u) : Ub + zoff[i] * NZp;
       bool xz = xzero;
@@ -806,6 +879,37 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
       if (BULK && (fl & 1u)) xz = true;
       double2* abrow = AB + zoff[i] * TZp;
       const int e_beg = zeb[i];
+      if constexpr (G::ZBAL) {
+        // balanced map: a whole item or half an element (warp-uniform per slot); ZS == 1
+        const unsigned part = (zpart >> (2 * i)) & 3u;
+        if (part != 0u) {
+          constexpr int H = K / 2;
+          const int e = e_beg, ez = ez0 + e;
+          const double wl = ((FULL && !LOW) || ez > 0) ? 1.0 : 0.0, wr = (FULL || ez < g.Ez) ? 1.0 : 0.0;
+          double L[K + 1], R[K + 1], oa[H], ob[H];
+#pragma unroll
+          for (int s = 0; s <= K; ++s) R[s] = row[K * e + K + s];
+          if (BULK && (fl & 4u) && e == TZE - 1) R[K] = 0.0;
+          if (BULK && (fl & 16u)) R[0] = 0.0;
+          if (part == 1u && i == 0) {  // rows {0, 1}: the vertex row gathers the left element
+#pragma unroll
+            for (int s = 0; s < K; ++s) L[s] = row[K * e + s];
+            L[K] = R[0];
+            if (BULK && (fl & 2u)) L[0] = 0.0;
+            elem2_half<K, true>(cf, L, R, wl, wr, oa, ob);
+          } else {
+            elem2_half<K, false>(cf, L, R, wl, wr, oa, ob);
+          }
+          if (BULK && xz) {
+#pragma unroll
+            for (int r = 0; r < H; ++r) oa[r] = ob[r] = 0.0;
+          }
+          const int zl0 = K * e + ((part == 1u && i == 0) ? 0 : H);
+#pragma unroll
+          for (int r = 0; r < H; ++r) abrow[zl0 + r] = make_double2(oa[r], ob[r]);
+          continue;
+        }
+      }
       double L[K + 1], R[K + 1];
 #pragma unroll
       for (int s = 0; s <= K; ++s) L[s] = row[K * e_beg + s];
@@ -919,14 +1023,23 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   // column as compile-time register operands
   auto xphase_r = [&](auto RC, int x, auto MCP) {
     const int mc = parity_of(MCP);
-    constexpr int RR = decltype(RC)::value;
     const double2* MC = reinterpret_cast<const double2*>(MCs + mc * 2 * G::MC_SZ);
-    constexpr int r_loc = RR;
+    const int r_loc = parity_of(RC);  // compile-time for an IC<r>
     double cmx[K + 1], ckx[K + 1];
+    if constexpr (std::is_same_v<decltype(RC), int>) {
+      // one copy of the X-phase: the x-table column comes from constant memory by the (uniform)
+      // plane index instead of five unrolled copies with register operands
 #pragma unroll
-    for (int s = 0; s <= K; ++s) {
-      cmx[s] = cf.m(s, RR);
-      ckx[s] = cf.s(s, RR);
+      for (int s = 0; s <= K; ++s) {
+        cmx[s] = c_hat[K - 1][0][r_loc][s];
+        ckx[s] = c_hat[K - 1][1][r_loc][s];
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s <= K; ++s) {
+        cmx[s] = cf.m(s, parity_of(RC));
+        ckx[s] = cf.s(s, parity_of(RC));
+      }
     }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -1037,6 +1150,10 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   };
   auto xphase = [&](int x, auto mc) {
     const int r_loc = xdeg ? 0 : x - K * ecur;   // 0..K
+    if constexpr (SPK_XR_RUNTIME) {
+      xphase_r(r_loc, x, mc);
+      return;
+    }
     switch (r_loc) {
       case 0: xphase_r(IC<0>{}, x, mc); break;
       case 1: xphase_r(IC<1>{}, x, mc); break;
@@ -1051,14 +1168,15 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
   // unrolled by two so every buffer address is a compile-time offset.
   // split barrier: interval t waits for interval t-1's arrivals; MA/C plane t lives in buffer t % 3
   auto interval_split = [&](auto P, int t) {
-    constexpr int p = decltype(P)::value;  // == t & 1
+    const auto p = P;  // == t & 1: a compile-time IC<p> (loop unrolled by two) or a runtime int
+    const auto p1 = other_parity(P);
     if (t >= 1) mbar_wait(ibar, static_cast<unsigned>(t - 1) & 1u);
     if constexpr (BULK) {
-      if (t < nplanes) mbar_wait(&ubar[p], static_cast<unsigned>(t >> 1) & 1u);
+      if (t < nplanes) mbar_wait(&ubar[parity_of(p)], static_cast<unsigned>(t >> 1) & 1u);
     }
-    if (t + 1 < nplanes) load_plane(xs + t + 1, IC<1 - p>{});
-    if (t < nplanes) zphase(IC<p>{}, xs + t);
-    if (t >= 1 && t - 1 < nplanes) yphase(IC<1 - p>{}, (t - 1) % 3);
+    if (t + 1 < nplanes) load_plane(xs + t + 1, p1);
+    if (t < nplanes) zphase(p, xs + t);
+    if (t >= 1 && t - 1 < nplanes) yphase(p1, (t - 1) % 3);
     cp_async_wait_all();  // this thread's part of plane t+1 has landed
     if constexpr (SPK_WARP_ARRIVE) {
       // one arrival per warp: every arrival wakes the threads sleeping in the barrier wait
@@ -1104,9 +1222,13 @@ __device__ __forceinline__ void stage_apply_body(const SpkApplyArgs& a, const Sp
     }
     cp_async_wait_all();
     __syncthreads();  // plane 0 in shared memory, barrier initialised
-    for (int t = 0; t < nplanes + 2; t += 2) {
-      interval_split(IC<0>{}, t);
-      if (t + 1 < nplanes + 2) interval_split(IC<1>{}, t + 1);
+    if constexpr (SPK_SPLIT_UNROLL2) {
+      for (int t = 0; t < nplanes + 2; t += 2) {
+        interval_split(IC<0>{}, t);
+        if (t + 1 < nplanes + 2) interval_split(IC<1>{}, t + 1);
+      }
+    } else {  // one copy of the interval (half the hot loop's instruction footprint)
+      for (int t = 0; t < nplanes + 2; ++t) interval_split(t & 1, t);
     }
     __syncthreads();
   } else if constexpr (UNROLL2) {
