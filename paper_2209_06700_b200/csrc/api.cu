@@ -215,6 +215,9 @@ void set_chunking(const spk_ctx* c, SpkApplyArgs& a, int K, int nb, int Qcta) {
   }
   a.xe_chunk = (int)((nel + nch - 1) / nch);
   a.nchunks = (nel + a.xe_chunk - 1) / a.xe_chunk;
+  // automatic chunking of plain launches: the launcher refines the count with the instantiation's
+  // resident-CTA slots (stage_apply.cuh rechunk)
+  a.chunk_auto = (c->target_ctas <= 0 && a.vplanes == 0) ? 1 : 0;
 }
 
 SpkApplyArgs base_args(const spk_ctx* c, int level) {

@@ -45,6 +45,7 @@ struct SpkApplyArgs {
   long long su, sv;
   SpkDims g;
   int xe_chunk, nchunks;  // x-chunking of the sliding window
+  int chunk_auto;         // host: the launcher may re-chunk with the kernel's real occupancy
   int ex_begin, ex_end;   // element range in x whose nodes are produced (slab windows)
   int store_last;         // also produce the last vertex plane when ex_end == Ex
   // virtual x-split (block mode): the CTA's Q "blocks" are Q consecutive x-ranges of ONE block,

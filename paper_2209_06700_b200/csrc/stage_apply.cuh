@@ -1519,6 +1519,16 @@ const unsigned char* ztail_order() {
   return tab;
 }
 
+// SPK_CHUNK_MODEL=0: keep the host's fixed-target chunk count
+inline bool spk_chunk_model() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SPK_CHUNK_MODEL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
 template <int K, int Q, bool BLOCK, int EPI>
 cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out) {
   using G = Geo<K, Q>;
@@ -1570,6 +1580,39 @@ cudaError_t launch_one(const SpkApplyArgs& a_in, cudaStream_t s, int* nctas_out)
   const int gz = (a.g.Ez + 1 + G::TZE - 1) / G::TZE;
   const int gy = a.g.Ey == 0 ? 1 : (a.g.Ey + 1 + G::TYE - 1) / G::TYE;
   const int nb = BLOCK ? a.nblk / Q : 1;  // CTA groups of Q blocks
+  // x-chunk count by a makespan model over the instantiation's resident CTA slots: rounds of CTAs x
+  // plane intervals per CTA (chunk planes + halo element + pipeline fill). The fixed "four waves of
+  // 148" target ran C5's k = 3 operator (169 tiles) as 676 CTAs = 2.3 waves on 296 slots: 249 us
+  // against 213 us with five chunks (2.85 waves); k = 4 / k = 2 at 289 tiles are flat in the count.
+  static int slots = -1;
+  if (slots < 0) {
+    int occ = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, smem) != cudaSuccess) occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = occ * sms;
+  }
+  if (a.chunk_auto && a.g.Ex > 0 && slots > 0 && spk_chunk_model()) {
+    const long long tiles = (long long)gz * gy * nb;
+    const int nel = a.ex_end - a.ex_begin;
+    // (large levels keep at least ~two rounds: the tiles are not uniform -- boundary tiles run the
+    // generic body, the last tile row / column is thin -- and a single round of long CTAs measured
+    // worse than two or three: C2 constrained 402 -> 450 us)
+    const bool big = tiles * (nel / 4) >= 2LL * slots;
+    long long best = -1;
+    int best_xe = a.xe_chunk;
+    for (int nch = 1; nch <= nel && nch <= 64; ++nch) {
+      const int xe = (nel + nch - 1) / nch;
+      if (xe < 2 && nel >= 2) break;
+      const int n2 = (nel + xe - 1) / xe;
+      if (big && tiles * n2 * 20 < 38LL * slots) continue;
+      const long long rounds = (tiles * n2 + slots - 1) / slots;
+      const long long cost = rounds * ((long long)xe * K + K + 3);
+      if (best < 0 || cost < best) { best = cost; best_xe = xe; }
+    }
+    a.xe_chunk = best_xe;
+    a.nchunks = (nel + best_xe - 1) / best_xe;
+  }
   // the plane loads address a CTA's Q stage rows with 32-bit byte offsets from its first row
   if (((long long)(Q - 1) * a.su + a.g.n) * 8 > 0xFFFFFFFFLL) return cudaErrorInvalidValue;
   dim3 grid(gz, gy, a.nchunks * nb);
