@@ -36,6 +36,7 @@ struct spk_ctx {
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
+  int mgs_pair = 1;                  // paired MGS sweeps for large vectors (SPK_MGS_PAIR)
   int mgs_coop = 1;                  // cooperative single-launch MGS column for small vectors (SPK_MGS_COOP)
   long long mgs_coop_max = 1LL << 25; // ... up to this many doubles (measured: C5 -5 %, C4 at 68M neutral)
   long long cv_max_nodes = 2200;  // fused coarse V-cycle: top level up to this many nodes (SPK_CV_MAXN;
@@ -400,6 +401,7 @@ int spk_ctx_create(int dim, int max_level, int degree, spk_ctx** out) {
   if (const char* e = std::getenv("SPK_FUSE_RESTRICT_MAX")) c->fuse_restrict_max = std::atoll(e);
   if (const char* e = std::getenv("SPK_CV_MAXN")) c->cv_max_nodes = std::atoll(e);
   if (const char* e = std::getenv("SPK_MGS_COOP")) c->mgs_coop = std::atoi(e);
+  if (const char* e = std::getenv("SPK_MGS_PAIR")) c->mgs_pair = std::atoi(e);
   if (const char* e = std::getenv("SPK_MGS_COOP_MAX")) c->mgs_coop_max = std::atoll(e);
   c->dim = dim;
   c->max_level = max_level;
@@ -1095,6 +1097,27 @@ int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, d
     for (int i = 0; i <= j; ++i) a.basis[i] = basis[i];
     cudaError_t e = spk_launch_mgs_column_coop(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "mgs_column_coop");
+    return SPK_OK;
+  }
+  if (c->mgs_pair && j >= 1) {
+    // paired sweeps (vecops.cu mgs2_kernel): pairs (v0, v1), (v2, v3), ...; sweep p applies pair
+    // p - 1's updates and takes pair p's dots; the last sweep applies the last pair and takes ||w||
+    if (int rc = ensure_scratch(c, 3 * spk_mgs_grid())) return rc;
+    const int nv = j + 1;
+    for (int i0 = 0; i0 < nv + 2; i0 += 2) {  // i0: first vector of the current pair (>= nv: norm)
+      SpkMgs2Args a;
+      std::memset(&a, 0, sizeof(a));
+      a.n = n; a.w = w; a.partial = c->partial; a.counter = c->counter;
+      a.np = i0 == 0 ? 0 : std::min(2, nv - (i0 - 2));
+      for (int k = 0; k < a.np; ++k) { a.vp[k] = basis[i0 - 2 + k]; a.hp[k] = hcol + i0 - 2 + k; }
+      a.nc = i0 >= nv ? 0 : std::min(2, nv - i0);
+      for (int k = 0; k < a.nc; ++k) { a.vc[k] = basis[i0 + k]; a.out[k] = hcol + i0 + k; }
+      if (a.nc == 0) a.out[0] = hcol + nv;
+      cudaError_t e = spk_launch_mgs2(a, (cudaStream_t)stream);
+      if (e != cudaSuccess) return cuda_fail(e, "mgs2");
+      if (a.nc == 0) break;
+    }
+    if (v_next) return spk_scale_div(n, w, hcol + j + 1, v_next, stream);
     return SPK_OK;
   }
   int rc = spk_mgs(c, n, w, nullptr, nullptr, basis[0], hcol, stream);

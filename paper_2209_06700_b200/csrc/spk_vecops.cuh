@@ -84,6 +84,21 @@ struct SpkMgsArgs {
   int sq;  // v_cur == null: 1 -> *out = sum w^2 (a rank's partial, all-reduced by the caller), 0 -> ||w||
 };
 
+// paired MGS sweep: w -= h0 v_prev0 + h1 v_prev1 (in that order), then the dots of w with up to two
+// further basis vectors and their mutual dot (or ||w||)
+struct SpkMgs2Args {
+  long long n;
+  double* w;
+  const double* vp[2];
+  const double* hp[2];
+  const double* vc[2];
+  int np, nc;
+  double* out[2];
+  double* partial;   // 3 x grid
+  unsigned* counter;
+};
+cudaError_t spk_launch_mgs2(const SpkMgs2Args& a, cudaStream_t s);
+
 struct SpkSepArgs {
   SpkDims g;
   const double* gx;

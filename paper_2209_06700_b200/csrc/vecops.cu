@@ -700,6 +700,127 @@ __global__ void __launch_bounds__(TPB) mgs_kernel(const __grid_constant__ SpkMgs
   finalize_partials(block_sum(mine, red), a.partial, a.counter, a.out, a.v_cur == nullptr && !a.sq, red);
 }
 
+// ---- paired MGS sweep (large vectors): two Gram-Schmidt steps per pass over w ----
+// Modified Gram-Schmidt (krylov.py:74-82) takes h_a = <w, v_a>, w -= h_a v_a, h_b = <w, v_b>. With
+// s_a = <w, v_a>, s_b = <w, v_b>, c = <v_a, v_b> of the SAME w, h_a = s_a and h_b = s_b - h_a c is the
+// same number in exact arithmetic (the basis' own loss of orthogonality c ~ 1e-16 is kept, not
+// assumed zero), so a sweep handles two basis vectors: it applies the previous pair's updates (in
+// MGS order) and accumulates the three dots. Passes over memory per pair: w read + write, two
+// vectors for the update, two for the dots = 6 instead of 8.
+template <int NP, int NC>
+__device__ __forceinline__ void mgs2_body(const SpkMgs2Args& a, double h0, double h1, double (&out)[3]) {
+  double* __restrict__ w = a.w;
+  const double* __restrict__ p0 = a.vp[0];
+  const double* __restrict__ p1 = a.vp[1];
+  const double* __restrict__ c0 = a.vc[0];
+  const double* __restrict__ c1 = a.vc[1];
+  const long long n = a.n;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  double sa[4] = {0, 0, 0, 0}, sb[4] = {0, 0, 0, 0}, sc[4] = {0, 0, 0, 0};
+  uintptr_t al = reinterpret_cast<uintptr_t>(w);
+  if (NP >= 1) al |= reinterpret_cast<uintptr_t>(p0);
+  if (NP >= 2) al |= reinterpret_cast<uintptr_t>(p1);
+  if (NC >= 1) al |= reinterpret_cast<uintptr_t>(c0);
+  if (NC >= 2) al |= reinterpret_cast<uintptr_t>(c1);
+  long long done = 0;
+  auto one = [&](double wv, double pa, double pb, double ca, double cb, int k) {
+    if (NP >= 1) wv = wv - h0 * pa;
+    if (NP >= 2) wv = wv - h1 * pb;
+    if (NC == 0) sa[k] = fma(wv, wv, sa[k]);
+    if (NC >= 1) sa[k] = fma(ca, wv, sa[k]);
+    if (NC >= 2) {
+      sb[k] = fma(cb, wv, sb[k]);
+      sc[k] = fma(ca, cb, sc[k]);
+    }
+    return wv;
+  };
+  if ((al & 15) == 0) {
+    const long long n2 = n / 2;
+    double2* __restrict__ w2 = reinterpret_cast<double2*>(w);
+    const double2* __restrict__ p02 = reinterpret_cast<const double2*>(p0);
+    const double2* __restrict__ p12 = reinterpret_cast<const double2*>(p1);
+    const double2* __restrict__ c02 = reinterpret_cast<const double2*>(c0);
+    const double2* __restrict__ c12 = reinterpret_cast<const double2*>(c1);
+    const double2 z = make_double2(0.0, 0.0);
+    // one 16-byte pair of every vector per thread and iteration, all reads streaming (evict-first):
+    // measured 6.4 TB/s on the five-read / one-write sweep; two pairs per thread (grid-strided or
+    // adjacent) ran at 5.7 TB/s
+    long long i = tid;
+    for (; i < n2; i += nth) {
+      double2 wa = w2[i];
+      double2 pa0 = z, pa1 = z, ca0 = z, ca1 = z;
+      if (NP >= 1) pa0 = __ldcs(p02 + i);
+      if (NP >= 2) pa1 = __ldcs(p12 + i);
+      if (NC >= 1) ca0 = __ldcs(c02 + i);
+      if (NC >= 2) ca1 = __ldcs(c12 + i);
+      wa.x = one(wa.x, pa0.x, pa1.x, ca0.x, ca1.x, 0);
+      wa.y = one(wa.y, pa0.y, pa1.y, ca0.y, ca1.y, 1);
+      if (NP >= 1) w2[i] = wa;
+    }
+    done = 2 * n2;
+  }
+  for (long long i = done + tid; i < n; i += nth) {
+    const double wv = one(w[i], NP >= 1 ? p0[i] : 0.0, NP >= 2 ? p1[i] : 0.0, NC >= 1 ? c0[i] : 0.0,
+                          NC >= 2 ? c1[i] : 0.0, 0);
+    if (NP >= 1) w[i] = wv;
+  }
+  out[0] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+  out[1] = (sb[0] + sb[1]) + (sb[2] + sb[3]);
+  out[2] = (sc[0] + sc[1]) + (sc[2] + sc[3]);
+}
+
+__global__ void __launch_bounds__(TPB, 4) mgs2_kernel(const __grid_constant__ SpkMgs2Args a) {
+  spk_pdl_wait();
+  spk_pdl_trigger();
+  __shared__ double red[TPB];
+  __shared__ bool last;
+  const double h0 = a.np >= 1 ? *a.hp[0] : 0.0, h1 = a.np >= 2 ? *a.hp[1] : 0.0;
+  double mine[3];
+  switch (a.np * 3 + a.nc) {
+    case 0: mgs2_body<0, 0>(a, h0, h1, mine); break;
+    case 1: mgs2_body<0, 1>(a, h0, h1, mine); break;
+    case 2: mgs2_body<0, 2>(a, h0, h1, mine); break;
+    case 3: mgs2_body<1, 0>(a, h0, h1, mine); break;
+    case 4: mgs2_body<1, 1>(a, h0, h1, mine); break;
+    case 5: mgs2_body<1, 2>(a, h0, h1, mine); break;
+    case 6: mgs2_body<2, 0>(a, h0, h1, mine); break;
+    case 7: mgs2_body<2, 1>(a, h0, h1, mine); break;
+    default: mgs2_body<2, 2>(a, h0, h1, mine); break;
+  }
+  // last-CTA-done finalisation of the three sums, partials summed in CTA order (deterministic)
+  const int nsum = a.nc == 2 ? 3 : 1;
+  for (int k = 0; k < nsum; ++k) {
+    const double bs = block_sum(mine[k], red);
+    __syncthreads();
+    if (threadIdx.x == 0) a.partial[(long long)k * gridDim.x + blockIdx.x] = bs;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(a.counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double tot[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < nsum; ++k) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      s += ((volatile double*)a.partial)[(long long)k * gridDim.x + b];
+    tot[k] = block_sum(s, red);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (a.nc == 0) *a.out[0] = sqrt(tot[0]);
+    else {
+      *a.out[0] = tot[0];
+      if (a.nc == 2) *a.out[1] = tot[1] - tot[0] * tot[2];
+    }
+    *a.counter = 0u;
+  }
+}
+
 // ---- one MGS column in one cooperative launch (small vectors: each of the j+2 separate launches is
 //      latency-bound there). Same sweeps (mgs_body); the per-CTA partials are summed by every CTA in
 //      CTA order after a grid barrier (run-to-run deterministic); partials double-buffered by step.
@@ -1131,6 +1252,10 @@ cudaError_t spk_launch_combine(const SpkCombineArgs& a, cudaStream_t s) {
 }
 
 int spk_mgs_grid() { return 148 * 8; }
+
+cudaError_t spk_launch_mgs2(const SpkMgs2Args& a, cudaStream_t s) {
+  return spk_launch(mgs2_kernel, spk_mgs_grid(), TPB, 0, s, a);
+}
 
 cudaError_t spk_launch_mgs(const SpkMgsArgs& a, cudaStream_t s) {
   return spk_launch(mgs_kernel, spk_mgs_grid(), TPB, 0, s, a);
