@@ -36,7 +36,7 @@ struct spk_ctx {
   int target_ctas = 0;    // 0: automatic x-chunking
   int fill_wave = 1;      // automatic chunking may shorten chunks to fill one wave (SPK_FILL_WAVE=0: off)
   int fuse_transfer = 1;  // fused 3D prolongation on whole-mesh levels (SPK_FUSE_TRANSFER=0: three sweeps)
-  int mgs_pair = 1;                  // paired MGS sweeps for large vectors (SPK_MGS_PAIR)
+  int mgs_pair = 3;                  // paired MGS sweeps: bit 0 large vectors, bit 1 cooperative column (SPK_MGS_PAIR)
   int mgs_coop = 1;                  // cooperative single-launch MGS column for small vectors (SPK_MGS_COOP)
   long long mgs_coop_max = 1LL << 25; // ... up to this many doubles (measured: C5 -5 %, C4 at 68M neutral)
   long long cv_max_nodes = 2200;  // fused coarse V-cycle: top level up to this many nodes (SPK_CV_MAXN;
@@ -1090,16 +1090,17 @@ int spk_mgs_column(spk_ctx* c, long long n, int j, const double* const* basis, d
   if (j < 0 || !basis || !w || !hcol) return fail(SPK_ECONFIG, "mgs_column: bad arguments");
   // small vectors: the whole column in one cooperative launch (the j+2 launches are latency-bound)
   if (c->mgs_coop && n <= c->mgs_coop_max && j + 1 < SPK_MGS_MAXCOL) {
-    if (int rc = ensure_scratch(c, 2 * spk_mgs_coop_grid())) return rc;
+    if (int rc = ensure_scratch(c, 6 * spk_mgs_coop_grid())) return rc;
     SpkMgsColArgs a;
     std::memset(&a, 0, sizeof(a));
     a.n = n; a.j = j; a.w = w; a.hcol = hcol; a.v_next = v_next; a.partial = c->partial;
+    a.pair = (c->mgs_pair & 2) ? 1 : 0;  // SPK_MGS_PAIR bit 1: paired sweeps in the cooperative column too
     for (int i = 0; i <= j; ++i) a.basis[i] = basis[i];
     cudaError_t e = spk_launch_mgs_column_coop(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "mgs_column_coop");
     return SPK_OK;
   }
-  if (c->mgs_pair && j >= 1) {
+  if ((c->mgs_pair & 1) && j >= 1) {
     // paired sweeps (vecops.cu mgs2_kernel): pairs (v0, v1), (v2, v3), ...; sweep p applies pair
     // p - 1's updates and takes pair p's dots; the last sweep applies the last pair and takes ||w||
     if (int rc = ensure_scratch(c, 3 * spk_mgs_grid())) return rc;

@@ -59,7 +59,8 @@ struct SpkMgsColArgs {  // one MGS column (spk_mgs_column) in one cooperative la
   double* w;
   double* hcol;     // H[0 .. j+1, j]
   double* v_next;   // w / H[j+1, j] (optional)
-  double* partial;  // 2 * grid doubles
+  double* partial;  // 2 * grid doubles (paired: 6 * grid)
+  int pair;         // paired sweeps (two basis vectors per grid barrier)
   const double* basis[SPK_MGS_MAXCOL];
 };
 

@@ -827,6 +827,68 @@ __global__ void __launch_bounds__(TPB, 4) mgs2_kernel(const __grid_constant__ Sp
 __global__ void __launch_bounds__(TPB) mgs_column_coop_kernel(const __grid_constant__ SpkMgsColArgs c) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[TPB];
+  if (c.pair) {
+    // paired sweeps (mgs2_body): half the grid barriers per column
+    SpkMgs2Args a2;
+    a2.n = c.n;
+    a2.w = c.w;
+    const int nv = c.j + 1;
+    double h0 = 0.0, h1 = 0.0, hlast = 0.0;
+    for (int i0 = 0, step = 0;; i0 += 2, ++step) {
+      const int np = i0 == 0 ? 0 : min(2, nv - (i0 - 2));
+      const int nc = i0 >= nv ? 0 : min(2, nv - i0);
+      a2.np = np;
+      a2.nc = nc;
+      for (int k = 0; k < 2; ++k) {
+        a2.vp[k] = k < np ? c.basis[i0 - 2 + k] : nullptr;
+        a2.vc[k] = k < nc ? c.basis[i0 + k] : nullptr;
+      }
+      double mine[3];
+      switch (np * 3 + nc) {
+        case 0: mgs2_body<0, 0>(a2, h0, h1, mine); break;
+        case 1: mgs2_body<0, 1>(a2, h0, h1, mine); break;
+        case 2: mgs2_body<0, 2>(a2, h0, h1, mine); break;
+        case 3: mgs2_body<1, 0>(a2, h0, h1, mine); break;
+        case 4: mgs2_body<1, 1>(a2, h0, h1, mine); break;
+        case 5: mgs2_body<1, 2>(a2, h0, h1, mine); break;
+        case 6: mgs2_body<2, 0>(a2, h0, h1, mine); break;
+        case 7: mgs2_body<2, 1>(a2, h0, h1, mine); break;
+        default: mgs2_body<2, 2>(a2, h0, h1, mine); break;
+      }
+      const int nsum = nc == 2 ? 3 : 1;
+      double* part = c.partial + (step & 1) * 3 * gridDim.x;
+      for (int k = 0; k < nsum; ++k) {
+        const double bs = block_sum(mine[k], red);
+        __syncthreads();
+        if (threadIdx.x == 0) part[k * gridDim.x + blockIdx.x] = bs;
+      }
+      grid.sync();
+      double tot[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < nsum; ++k) {
+        double sp = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) sp += part[k * gridDim.x + b];
+        tot[k] = block_sum(sp, red);
+        __syncthreads();
+      }
+      if (nc == 0) {
+        hlast = sqrt(tot[0]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) c.hcol[nv] = hlast;
+        break;
+      }
+      h0 = tot[0];
+      h1 = nc == 2 ? tot[1] - tot[0] * tot[2] : 0.0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c.hcol[i0] = h0;
+        if (nc == 2) c.hcol[i0 + 1] = h1;
+      }
+    }
+    if (c.v_next) {
+      for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < c.n;
+           k += (long long)gridDim.x * blockDim.x)
+        c.v_next[k] = c.w[k] / hlast;
+    }
+    return;
+  }
   SpkMgsArgs a;
   a.sq = 0;
   a.n = c.n;
