@@ -11,7 +11,9 @@
 // M = h^d M_hat, K = h^(d-2) K_hat, so the host passes DM' = h^d DM and DK' = h^(d-2) DK.
 //
 // Schedule ("2.5D sliding window", one CTA = one (y,z) tile x one x-chunk, all Q stages):
-//   per x-plane:  cp.async plane x+1 into the other smem buffer (double buffering)
+//   per x-plane:  plane x+1 into the other smem buffer (double buffering): TMA boxes completing on an
+//                 mbarrier for interior tiles (load_plane_tma), per-node cp.async with zero-fill for
+//                 the ragged tiles on the high side
 //                 Z-phase   a = Mz u, b = Kz u                 (smem -> smem, 2 elements / item)
 //                 Y-phase   ma = My a, c = Ky a + My b          (smem -> smem, 2 elements / item)
 //                 X-phase   stage mix p_i = sum_j DM_ij ma_j + DK_ij c_j, q_i = sum_j DK_ij ma_j
