@@ -744,8 +744,8 @@ __device__ __forceinline__ void mgs2_body(const SpkMgs2Args& a, double h0, doubl
     const double2* __restrict__ c12 = reinterpret_cast<const double2*>(c1);
     const double2 z = make_double2(0.0, 0.0);
     // one 16-byte pair of every vector per thread and iteration, all reads streaming (evict-first):
-    // measured 6.4 TB/s on the five-read / one-write sweep; two pairs per thread (grid-strided or
-    // adjacent) ran at 5.7 TB/s
+    // measured 6.4 TB/s on the five-read / one-write sweep; two pairs per thread (grid-strided, adjacent,
+    // or grid-strided with streaming loads and stores) ran at 5.7-6.3 TB/s
     long long i = tid;
     for (; i < n2; i += nth) {
       double2 wa = w2[i];

@@ -33,10 +33,12 @@ def test_coarse_vcycle_and_k1_bitwise_repeatable():
         assert torch.equal(h.apply_stage_operator(4, DM, DK, u), vref), i
 
 
-@pytest.mark.parametrize("n", [5000, 1 << 20])
-def test_mgs_column_bitwise_repeatable(n):
+@pytest.mark.parametrize("n,j", [(5000, 6), (1 << 20, 6), (1 << 20, 5), ((1 << 25) + 9, 6), ((1 << 25) + 9, 3)])
+def test_mgs_column_bitwise_repeatable(n, j):
+    # (n <= 2^25: the cooperative single-launch column; above: the paired sweeps of mgs2_kernel. The
+    # basis here is NOT orthogonal, so the paired form's correction h_b = s_b - h_a <v_a, v_b> is
+    # exercised with a large mutual dot; odd and even numbers of basis vectors)
     g = torch.Generator(device="cuda").manual_seed(6)
-    j = 6
     basis = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) for _ in range(j + 1)]
     w0 = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
     ptrs = (_lib.ctypes.c_void_p * (j + 1))(*[b.data_ptr() for b in basis])
